@@ -1,0 +1,106 @@
+/*
+ * attn2d_sm100 — C ABI of the B200 (sm_100a) 2D-Attention hot path.
+ *
+ * Drop-in boundary for the reference operator API of
+ * /root/reference/pkg/src/attn2d (a Python package; its "FFI" is a Python
+ * call, so the binding a maintainer adds is a ctypes shim — INTEGRATION.md).
+ * Each entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *  - All tensor arguments are DEVICE pointers; shapes/sizes are plain ints.
+ *  - bf16 tensors are head-major and contiguous: q/out [H][T][D],
+ *    k/v [H_kv][T][D] (the reference's DenseTensor.values layout, oracle.py:15-34).
+ *  - Positions are int32 original token indices, one per token (DenseTensor.positions).
+ *  - LSE is the natural-log log-sum-exp (oracle.py:53-66), fp32 [H][T].
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *    stream-ordered and never synchronise the host.
+ *  - Return 0 on success; non-zero on error with a message in
+ *    a2d_last_error() (thread-local). Invalid shapes return A2D_EINVAL, the
+ *    analogue of the reference's ValueError.
+ */
+#ifndef ATTN2D_SM100_H_
+#define ATTN2D_SM100_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define A2D_OK 0
+#define A2D_EINVAL 1
+#define A2D_ECUDA 2
+
+/* Thread-local message of the last failing call. */
+const char* a2d_last_error(void);
+/* ABI version (bumped on any signature change). */
+int a2d_abi_version(void);
+
+/* Per-tile (min, max) of positions: out[2*t], out[2*t+1] for tile t of
+ * `tile` tokens; empty tiles get (INT_MAX, INT_MIN). Input to the
+ * attention entry points (tile = 128 for keys and forward queries, 64 for
+ * backward queries). */
+int a2d_tile_bounds(const int32_t* pos, int64_t T, int32_t tile, int32_t* out_minmax, void* stream);
+
+/* One ring step forward: attention of a query chunk against one KV chunk.
+ * Replaces ref attention_block (oracle.py:97-101) and, with merge=1, the
+ * fold block_update(acc, blk) (oracle.py:111-124) of run_double_ring
+ * (ring.py:64-79).
+ *   merge=0: lse := blk.lse; acc_o (fp32, nullable) := blk.out;
+ *            out_bf16 (nullable) := bf16(blk.out)
+ *   merge=1: (acc_o, lse) := block_update((acc_o, lse), blk) in place;
+ *            out_bf16 (nullable) := bf16(new acc_o)
+ * D in {64, 128}; scale = 1/sqrt(d) of the caller's true head dim. GQA:
+ * head h reads KV head h / (H/H_kv) (oracle.py:45-50). */
+int a2d_fa_fwd_chunk(const void* q, const void* k, const void* v, const int32_t* q_pos, const int32_t* k_pos,
+                     const int32_t* q_bounds128, const int32_t* k_bounds128, int32_t H, int32_t H_kv, int64_t Tq,
+                     int64_t Tk, int32_t D, int32_t causal, float scale, int32_t merge, float* lse, float* acc_o,
+                     void* out_bf16, void* stream);
+
+/* Backward preprocess for a query chunk: delta[h][t] = sum_d dO*O (the
+ * reference's `row`, oracle.py:145) and lse2 = lse*log2(e) (+inf for rows
+ * with lse=-inf and for padding). Outputs are [H][Tq_pad], Tq_pad =
+ * round_up(Tq, 64). */
+int a2d_bwd_preprocess(const void* o, const void* dout, const float* lse, int32_t H, int64_t Tq, int32_t D,
+                       float* lse2, float* delta, void* stream);
+
+/* One ring step backward: gradients of the block (query chunk, KV chunk)
+ * given the FINAL lse/delta of the query rows. Replaces the per-block part
+ * of ref attention_backward (oracle.py:127-152):
+ *   dq_acc[H][Tq][D] (fp32) += dS K / sqrt(d)          (atomic accumulate)
+ *   dk, dv [H_kv][Tk][D] (fp32) (+)= partial (accumulate_kv selects +=)
+ * D must be 128 (pad smaller head dims with zeros and pass the true scale). */
+int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* dout, const int32_t* q_pos,
+                     const int32_t* k_pos, const int32_t* q_bounds64, const int32_t* k_bounds128, const float* lse2,
+                     const float* delta, float* dq_acc, float* dk, float* dv, int32_t accumulate_kv, int32_t H,
+                     int32_t H_kv, int64_t Tq, int64_t Tk, int32_t D, int32_t causal, float scale, void* stream);
+
+/* Standalone block_update (oracle.py:111-124) on rows of D fp32 values. */
+int a2d_merge(float* acc_o, float* acc_lse, const float* blk_o, const float* blk_lse, int64_t rows, int32_t D,
+              void* stream);
+
+/* dst[b][a][:] = src[a][b][:] for blocks of block_bytes (multiple of 16).
+ * With A = d_hp peers and B = local heads it is the SeqAlltoAll
+ * unpack/pack (ref seq_alltoall_scatter / gather, sharding.py:131-169). */
+int a2d_permute_blocks(const void* src, void* dst, int64_t A, int64_t B, int64_t block_bytes, void* stream);
+
+/* dst[i][:] = src[map[i]][:] — GQA KV replication by addressing
+ * (ref kv_replicate, sharding.py:109-128). map is a device int32 array. */
+int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, int64_t n, int64_t block_bytes, void* stream);
+
+/* dst[h] = sum_r src[h*rep + r] over per_head fp32 values (gradient of kv_replicate). */
+int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream);
+
+/* Elementwise helpers (n multiple of 4). */
+int a2d_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
+int a2d_add_f32(float* dst, const float* src, int64_t n, void* stream);
+
+/* UMMA plumbing self-test (one CTA, 128x128x128 bf16 GEMMs in four operand
+ * layouts); c is fp32 [4][128][128]. Used by the parity tests. */
+int a2d_selftest_umma(const void* a, const void* b, const void* v, const void* at, float* c, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ATTN2D_SM100_H_ */

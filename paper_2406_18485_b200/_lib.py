@@ -1,0 +1,70 @@
+"""ctypes binding of libattn2d_sm100.so (the C ABI in include/attn2d_sm100.h).
+
+There is deliberately no fallback: if the library is missing or fails to
+load, every op raises. The CPU oracle lives in ``oracle/`` and is test
+infrastructure only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libattn2d_sm100.so")
+
+_c_int, _c_i32, _c_i64, _c_f32, _vp = (ctypes.c_int, ctypes.c_int32, ctypes.c_int64,
+                                      ctypes.c_float, ctypes.c_void_p)
+
+# name -> argtypes (all return int status)
+SIGNATURES = {
+    "a2d_tile_bounds": [_vp, _c_i64, _c_i32, _vp, _vp],
+    "a2d_fa_fwd_chunk": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i64, _c_i64,
+                         _c_i32, _c_i32, _c_f32, _c_i32, _vp, _vp, _vp, _vp],
+    "a2d_bwd_preprocess": [_vp, _vp, _vp, _c_i32, _c_i64, _c_i32, _vp, _vp, _vp],
+    "a2d_fa_bwd_chunk": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                         _c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp],
+    "a2d_merge": [_vp, _vp, _vp, _vp, _c_i64, _c_i32, _vp],
+    "a2d_permute_blocks": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp],
+    "a2d_gather_blocks": [_vp, _vp, _vp, _c_i64, _c_i64, _vp],
+    "a2d_sum_replicas_f32": [_vp, _vp, _c_i64, _c_i32, _c_i64, _vp],
+    "a2d_f32_to_bf16": [_vp, _vp, _c_i64, _vp],
+    "a2d_add_f32": [_vp, _vp, _c_i64, _vp],
+    "a2d_selftest_umma": [_vp, _vp, _vp, _vp, _vp, _vp],
+}
+
+_lib = None
+
+
+class KernelError(RuntimeError):
+    """CUDA-side failure reported by the library."""
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the CDLL. Raises if the library is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} not built; run `python -m paper_2406_18485_b200.build` (no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = _c_int
+    lib.a2d_last_error.restype = ctypes.c_char_p
+    lib.a2d_last_error.argtypes = []
+    lib.a2d_abi_version.restype = _c_int
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke an entry point; map non-zero status to ValueError / KernelError."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.a2d_last_error().decode()
+        if rc == 1:
+            raise ValueError(msg)
+        raise KernelError(msg)

@@ -1,0 +1,238 @@
+// HBM-bound helper kernels around the attention GEMMs.
+//
+//  * tile_bounds     : per-tile (min,max) of the carried token positions; the
+//                      attention kernels classify tiles (skip / full / masked)
+//                      from these, so zig-zag chunks need no special casing.
+//  * bwd_preprocess  : delta = rowsum(dO * O) (the reference's `row`,
+//                      oracle.py:145) and lse2 = LSE*log2(e) (+inf for dead
+//                      rows and tail padding, so P = 0 there).
+//  * merge           : standalone block_update (oracle.py:111-124), K2.
+//  * permute_blocks  : [A][B][blk] -> [B][A][blk] byte copy with 128-bit
+//                      accesses; the pack / unpack around the head-parallel
+//                      all-to-all (sharding.py:131-169) are instances of it.
+//  * gather_blocks   : dst[i] = src[map[i]] (GQA replication without
+//                      materialising kv_replicate's copies, sharding.py:109-128).
+//  * sum_replicas    : gradient of that replication (sum of the copies).
+//  * cast kernels    : fp32 <-> bf16.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+#include <cmath>
+
+namespace a2d {
+
+__global__ void tile_bounds_kernel(const int* __restrict__ pos, int T, int tile, int2* __restrict__ out) {
+  const int t = blockIdx.x;
+  int lo = INT_MAX, hi = INT_MIN;
+  for (int i = t * tile + threadIdx.x; i < min(T, (t + 1) * tile); i += blockDim.x) {
+    const int v = pos[i];
+    lo = min(lo, v);
+    hi = max(hi, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ int slo[32], shi[32];
+  const int w = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) { slo[w] = lo; shi[w] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x / 32); ++i) { lo = min(lo, slo[i]); hi = max(hi, shi[i]); }
+    out[t] = make_int2(lo, hi);  // empty tile -> (INT_MAX, INT_MIN)
+  }
+}
+
+cudaError_t launch_tile_bounds(const int* pos, int T, int tile, int2* out, cudaStream_t s) {
+  const int n = (T + tile - 1) / tile;
+  if (n == 0) return cudaSuccess;
+  tile_bounds_kernel<<<n, 128, 0, s>>>(pos, T, tile, out);
+  return cudaGetLastError();
+}
+
+// One warp per query row; D = 128 or 64 bf16 elements.
+__global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                      int64_t o_sh, int64_t o_st, int64_t do_sh, int64_t do_st,
+                                      const float* __restrict__ lse, int H, int Tq, int Tq_pad, int D,
+                                      float* __restrict__ lse2, float* __restrict__ delta) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (warp >= H * Tq_pad) return;
+  const int h = warp / Tq_pad, t = warp % Tq_pad;
+  float acc = 0.f;
+  if (t < Tq) {
+    const __nv_bfloat16* po = o + h * o_sh + t * o_st;
+    const __nv_bfloat16* pd = dout + h * do_sh + t * do_st;
+    for (int c = lane * 2; c < D; c += 64) {
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(po + c));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pd + c));
+      acc += a.x * b.x + a.y * b.y;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    float l2 = INFINITY;
+    if (t < Tq) {
+      const float l = lse[(size_t)h * Tq + t];
+      l2 = l == -INFINITY ? INFINITY : l * 1.4426950408889634f;
+    }
+    lse2[(size_t)h * Tq_pad + t] = l2;
+    delta[(size_t)h * Tq_pad + t] = t < Tq ? acc : 0.f;
+  }
+}
+
+cudaError_t launch_bwd_preprocess(const __nv_bfloat16* o, const __nv_bfloat16* dout, int64_t o_sh, int64_t o_st,
+                                  int64_t do_sh, int64_t do_st, const float* lse, int H, int Tq, int Tq_pad,
+                                  int D, float* lse2, float* delta, cudaStream_t s) {
+  const int64_t warps = (int64_t)H * Tq_pad;
+  if (warps == 0) return cudaSuccess;
+  const int threads = 256;
+  const int64_t blocks = (warps * 32 + threads - 1) / threads;
+  bwd_preprocess_kernel<<<(unsigned)blocks, threads, 0, s>>>(o, dout, o_sh, o_st, do_sh, do_st, lse, H, Tq,
+                                                             Tq_pad, D, lse2, delta);
+  return cudaGetLastError();
+}
+
+// acc := block_update(acc, blk). acc_o fp32 [R][D]; blk_o bf16 or fp32.
+template <typename TB>
+__global__ void merge_kernel(float* __restrict__ acc_o, float* __restrict__ acc_lse, const TB* __restrict__ blk_o,
+                             const float* __restrict__ blk_lse, int64_t rows, int D) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float la = acc_lse[r], lb = blk_lse[r];
+  const float m = fmaxf(la, lb);
+  float wa = 0.f, wb = 0.f, ln = -INFINITY;
+  if (m != -INFINITY) {
+    const float ea = la == -INFINITY ? 0.f : expf(la - m);
+    const float eb = lb == -INFINITY ? 0.f : expf(lb - m);
+    const float z = ea + eb;
+    ln = m + logf(z);
+    wa = ea / z;
+    wb = eb / z;
+  }
+  for (int c = lane; c < D; c += 32) {
+    const float b = static_cast<float>(blk_o[r * D + c]);
+    acc_o[r * D + c] = acc_o[r * D + c] * wa + b * wb;
+  }
+  if (lane == 0) acc_lse[r] = ln;
+}
+
+cudaError_t launch_merge_f32(float* acc_o, float* acc_lse, const float* blk_o, const float* blk_lse, int64_t rows,
+                             int D, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  merge_kernel<float><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(acc_o, acc_lse, blk_o, blk_lse, rows, D);
+  return cudaGetLastError();
+}
+
+__global__ void permute_blocks_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t A, int64_t B,
+                                      int64_t blk_vec) {
+  const int64_t total = A * B * blk_vec;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i % blk_vec;
+    const int64_t ab = i / blk_vec;  // destination block index = b*A + a
+    const int64_t b = ab / A, a = ab % A;
+    dst[i] = __ldg(src + (a * B + b) * blk_vec + e);
+  }
+}
+
+// dst[b][a][:] = src[a][b][:], blocks of blk_bytes (multiple of 16).
+cudaError_t launch_permute_blocks(const void* src, void* dst, int64_t A, int64_t B, int64_t blk_bytes, int n_sm,
+                                  cudaStream_t s) {
+  if (blk_bytes % 16 != 0) return cudaErrorInvalidValue;
+  const int64_t total = A * B * (blk_bytes / 16);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = (int64_t)n_sm * 8;
+  if (blocks > cap) blocks = cap;
+  permute_blocks_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), A,
+                                                         B, blk_bytes / 16);
+  return cudaGetLastError();
+}
+
+__global__ void gather_blocks_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                     const int* __restrict__ map, int64_t n, int64_t blk_vec) {
+  const int64_t total = n * blk_vec;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = i / blk_vec, e = i % blk_vec;
+    dst[i] = __ldg(src + (int64_t)map[blk] * blk_vec + e);
+  }
+}
+
+cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, int64_t n, int64_t blk_bytes, int n_sm,
+                                 cudaStream_t s) {
+  if (blk_bytes % 16 != 0) return cudaErrorInvalidValue;
+  const int64_t total = n * (blk_bytes / 16);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  gather_blocks_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), map,
+                                                        n, blk_bytes / 16);
+  return cudaGetLastError();
+}
+
+// dst[h][e] = sum_r src[h*rep + r][e]   (fp32)
+__global__ void sum_replicas_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t heads, int rep,
+                                    int64_t per_head) {
+  const int64_t total = heads * per_head;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = i / per_head, e = i % per_head;
+    float acc = 0.f;
+    for (int r = 0; r < rep; ++r) acc += src[(h * rep + r) * per_head + e];
+    dst[i] = acc;
+  }
+}
+
+cudaError_t launch_sum_replicas(const float* src, float* dst, int64_t heads, int rep, int64_t per_head, int n_sm,
+                                cudaStream_t s) {
+  const int64_t total = heads * per_head;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  sum_replicas_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, dst, heads, rep, per_head);
+  return cudaGetLastError();
+}
+
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = src[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    dst[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
+cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, int n_sm, cudaStream_t s) {
+  if (n % 4 != 0) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  if (n4 == 0) return cudaSuccess;
+  int64_t blocks = (n4 + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(src),
+                                                      reinterpret_cast<uint2*>(dst), n4);
+  return cudaGetLastError();
+}
+
+// dst (fp32) += src (fp32): the dK/dV accumulate-and-forward step (K4).
+__global__ void add_f32_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = dst[i];
+    const float4 b = src[i];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    dst[i] = a;
+  }
+}
+
+cudaError_t launch_add_f32(float* dst, const float* src, int64_t n, int n_sm, cudaStream_t s) {
+  if (n % 4 != 0) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  if (n4 == 0) return cudaSuccess;
+  int64_t blocks = (n4 + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  add_f32_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src),
+                                                  n4);
+  return cudaGetLastError();
+}
+
+}  // namespace a2d

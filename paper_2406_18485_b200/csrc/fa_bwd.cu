@@ -1,0 +1,374 @@
+// Chunk flash-attention backward for sm_100a (K3).
+//
+// Gradients of one ring step's block (Q chunk vs one KV chunk) given the
+// FINAL softmax statistics of the query rows (global LSE, and
+// delta = rowsum(dO * O) = the reference's row = sum(dP * P), oracle.py:145):
+//   P   = exp(S - LSE)               dP = dO V^T
+//   dS  = P * (dP - delta) / sqrt(d)
+//   dV += P^T dO    dK += dS^T Q    dQ += dS K
+// GQA: the CTA walks every query head of its KV head's group, so dK/dV sum
+// over the G sharing heads inside TMEM (ref oracle.py:149-151).
+//
+// One CTA = one 128-key tile of one KV head; it streams 64-row query tiles.
+// Everything is computed key-major ("transposed") so that the key tile owns
+// the 128 TMEM lanes:
+//   S^T  = K Q^T      (M=128 keys, N=64 q, K=d)   TMEM region b
+//   dP^T = V dO^T                                  TMEM region b
+//   dQ^T = K^T dS^T   (M=d, N=64 q, K=128 keys)    TMEM region b (over S^T)
+//   dV  += P^T dO     (M=128 keys, N=d, K=64 q)    TMEM [256,384)
+//   dK  += dS^T Q                                  TMEM [384,512)
+// P^T and dS^T go through shared memory in the SW128 K-major layout; the same
+// bytes are the MN-major B operand of dQ^T, so one copy serves both GEMMs.
+// Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 "WG-A" (P, dS), 8-11 "WG-B"
+// (drain dQ^T with fp32 reductions into dq_acc, overlapping dV/dK GEMMs).
+#include "sm100.cuh"
+#include "kernels.h"
+
+namespace a2d {
+
+namespace bwd {
+constexpr int BK = 128;  // keys per CTA
+constexpr int BQ = 64;   // queries per iteration
+constexpr int D = 128;
+constexpr int QST = 2;   // Q/dO stages
+constexpr int kThreads = 384;
+// smem layout (bytes, from 1 KB aligned base)
+constexpr int kK = 0;
+constexpr int kV = kK + BK * D * 2;              // 32 KB each
+constexpr int kQ = kV + BK * D * 2;              // QST x 16 KB
+constexpr int kDO = kQ + QST * BQ * D * 2;       // QST x 16 KB
+constexpr int kP = kDO + QST * BQ * D * 2;       // 2 x 16 KB  (P^T, [key][q])
+constexpr int kDS = kP + 2 * BK * BQ * 2;        // 2 x 16 KB  (dS^T)
+constexpr int kStats = kDS + 2 * BK * BQ * 2;    // QST x (lse2[64], delta[64])
+constexpr int kEnd = kStats + QST * 2 * BQ * 4;
+constexpr int kBytes = kEnd + 1024;
+}  // namespace bwd
+
+struct BwdBars {
+  uint64_t kv_full;
+  uint64_t qdo_full[bwd::QST], qdo_empty[bwd::QST];
+  uint64_t s_full[2], ds_full[2], dq_full[2], dq_empty[2], pds_free[2];
+  uint64_t dkv_full;
+  uint32_t tmem_base;
+};
+
+A2D_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_constant__ BwdParams p) {
+  using namespace bwd;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ BwdBars bars;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nkt = (p.Tk + BK - 1) / BK;
+  const int kt = nkt - 1 - (int)blockIdx.x;  // heavy-first for causal
+  const int hk = blockIdx.y;
+  const int key0 = kt * BK;
+  const int nqt = (p.Tq + BQ - 1) / BQ;
+  const int Tq_pad = nqt * BQ;
+  const int2 kb = p.k_bounds[kt];
+  const bool causal = p.causal != 0;
+  const int n_iter_max = p.G * nqt;
+
+  // live(i): query tile qt of head g = i / nqt sees at least one key of this tile
+  auto live = [&](int qt) {
+    const int2 qb = p.q_bounds[qt];
+    return qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.kv_full, 1);
+    for (int i = 0; i < QST; ++i) { mbar_init(&bars.qdo_full[i], 1); mbar_init(&bars.qdo_empty[i], 1); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.s_full[b], 1);
+      mbar_init(&bars.ds_full[b], 128);
+      mbar_init(&bars.dq_full[b], 1);
+      mbar_init(&bars.dq_empty[b], 128);
+      mbar_init(&bars.pds_free[b], 1);
+    }
+    mbar_init(&bars.dkv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars.tmem_base);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tm_q); tma_prefetch(&p.tm_k); tma_prefetch(&p.tm_v); tma_prefetch(&p.tm_do);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+
+  if (warp == 0) {
+    // -------------------------------------------------------------- producer
+    if (lane == 0) {
+      mbar_expect_tx(&bars.kv_full, 2 * BK * D * 2);
+      for (int c = 0; c < 2; ++c) {
+        tma_load_3d(smem + kK + c * 16384, &p.tm_k, &bars.kv_full, c * 64, key0, hk);
+        tma_load_3d(smem + kV + c * 16384, &p.tm_v, &bars.kv_full, c * 64, key0, hk);
+      }
+      int it = 0;
+      for (int i = 0; i < n_iter_max; ++i) {
+        const int g = i / nqt, qt = i % nqt;
+        if (!live(qt)) continue;
+        const int h = hk * p.G + g;
+        const int qs = it % QST;
+        mbar_wait(&bars.qdo_empty[qs], ((it / QST) & 1) ^ 1);
+        mbar_expect_tx(&bars.qdo_full[qs], 2 * BQ * D * 2 + 2 * BQ * 4);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_3d(smem + kQ + qs * BQ * D * 2 + c * 8192, &p.tm_q, &bars.qdo_full[qs], c * 64, qt * BQ, h);
+          tma_load_3d(smem + kDO + qs * BQ * D * 2 + c * 8192, &p.tm_do, &bars.qdo_full[qs], c * 64, qt * BQ, h);
+        }
+        float* st = reinterpret_cast<float*>(smem + kStats) + qs * 2 * BQ;
+        bulk_g2s(st, p.lse2 + (size_t)h * Tq_pad + qt * BQ, BQ * 4, &bars.qdo_full[qs]);
+        bulk_g2s(st + BQ, p.delta + (size_t)h * Tq_pad + qt * BQ, BQ * 4, &bars.qdo_full[qs]);
+        ++it;
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int n = 0;
+      for (int qt = 0; qt < nqt; ++qt) n += live(qt) ? 1 : 0;
+      n *= p.G;
+      constexpr uint32_t id_s = idesc_bf16(BK, BQ, false, false);   // S^T, dP^T
+      constexpr uint32_t id_kv = idesc_bf16(BK, D, false, true);    // dV, dK
+      constexpr uint32_t id_dq = idesc_bf16(D, BQ, true, true);     // dQ^T
+      const uint32_t sK = smem_u32(smem + kK), sV = smem_u32(smem + kV);
+      const uint32_t sQ = smem_u32(smem + kQ), sDO = smem_u32(smem + kDO);
+      const uint32_t sP = smem_u32(smem + kP), sDS = smem_u32(smem + kDS);
+      const uint32_t tDV = tmem + 256, tDK = tmem + 384;
+      auto issue_s = [&](int i) {  // S^T_i and dP^T_i into region i&1
+        const int b = i & 1, qs = i % QST;
+        const uint32_t tS = tmem + b * 128, tDP = tmem + b * 128 + 64;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t ka = (k / 4) * 16384 + (k % 4) * 32;
+          const uint32_t kq = qs * BQ * D * 2 + (k / 4) * 8192 + (k % 4) * 32;
+          umma_ss(tS, sdesc_sw128(sK + ka, 16, 1024), sdesc_sw128(sQ + kq, 16, 1024), id_s, k > 0);
+          umma_ss(tDP, sdesc_sw128(sV + ka, 16, 1024), sdesc_sw128(sDO + kq, 16, 1024), id_s, k > 0);
+        }
+      };
+      if (n > 0) {
+        mbar_wait(&bars.kv_full, 0);
+        for (int i = 0; i < 2 && i < n; ++i) {
+          mbar_wait(&bars.qdo_full[i % QST], (i / QST) & 1);
+          tc_fence_after();
+          issue_s(i);
+          umma_commit(&bars.s_full[i & 1]);
+        }
+        for (int i = 0; i < n; ++i) {
+          const int b = i & 1, qs = i % QST;
+          mbar_wait(&bars.ds_full[b], (i >> 1) & 1);
+          tc_fence_after();
+          // dQ^T_i = K^T dS^T_i -> region b columns [0, 64)
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_ss(tmem + b * 128, sdesc_sw128(sK + k * 2048, 16384, 1024),
+                    sdesc_sw128(sDS + b * 16384 + k * 2048, 8192, 1024), id_dq, k > 0);
+          umma_commit(&bars.dq_full[b]);
+          // dV += P^T dO ; dK += dS^T Q
+#pragma unroll
+          for (int k = 0; k < BQ / 16; ++k) {
+            const uint32_t kmn = qs * BQ * D * 2 + k * 2048;
+            umma_ss(tDV, sdesc_sw128(sP + b * 16384 + k * 32, 16, 1024), sdesc_sw128(sDO + kmn, 8192, 1024),
+                    id_kv, (i > 0 || k > 0) ? 1u : 0u);
+            umma_ss(tDK, sdesc_sw128(sDS + b * 16384 + k * 32, 16, 1024), sdesc_sw128(sQ + kmn, 8192, 1024),
+                    id_kv, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&bars.pds_free[b]);
+          umma_commit(&bars.qdo_empty[qs]);
+          if (i + 2 < n) {
+            mbar_wait(&bars.dq_empty[b], (i >> 1) & 1);
+            mbar_wait(&bars.qdo_full[(i + 2) % QST], ((i + 2) / QST) & 1);
+            tc_fence_after();
+            issue_s(i + 2);
+            umma_commit(&bars.s_full[b]);
+          }
+        }
+        umma_commit(&bars.dkv_full);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // -------------------------------------------------------------- WG-A: P, dS
+    const int wq = warp % 4;
+    const int r = wq * 32 + lane;  // key row in tile == TMEM lane
+    const int key = key0 + r;
+    const bool key_ok = key < p.Tk;
+    const int kpos = key_ok ? p.k_pos[key] : INT_MAX;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const float sl2 = p.scale_log2, scale = p.scale;
+    int it = 0;
+    for (int i = 0; i < n_iter_max; ++i) {
+      const int qt = i % nqt;
+      if (!live(qt)) continue;
+      const int2 qb = p.q_bounds[qt];
+      const bool full = !causal || kb.y <= qb.x;
+      const int b = it & 1, qs = it % QST;
+      mbar_wait(&bars.qdo_full[qs], (it / QST) & 1);  // stats landed (TMA done)
+      mbar_wait(&bars.s_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      float s[BQ], dp[BQ];
+      {
+        uint32_t rr[32];
+#pragma unroll
+        for (int c = 0; c < BQ / 32; ++c) {
+          tmem_ld32(tmem + lane_base + b * 128 + c * 32, rr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(rr[j]);
+          tmem_ld32(tmem + lane_base + b * 128 + 64 + c * 32, rr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) dp[c * 32 + j] = __uint_as_float(rr[j]);
+        }
+      }
+      const float* st = reinterpret_cast<const float*>(smem + kStats) + qs * 2 * BQ;
+      if (it >= 2) mbar_wait(&bars.pds_free[b], ((it - 2) >> 1) & 1);  // P/dS smem b reusable
+      uint8_t* prow = smem + kP + b * 16384;
+      uint8_t* dsrow = smem + kDS + b * 16384;
+      const int* qp = p.q_pos + qt * BQ;
+#pragma unroll
+      for (int c8 = 0; c8 < BQ / 8; ++c8) {
+        uint32_t pw[4], dw[4];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          float pv[2], dv[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = c8 * 8 + j + e;
+            bool keep = key_ok;
+            if (!full) keep = keep && (qt * BQ + c < p.Tq) && kpos <= __ldg(qp + c);
+            const float pr = keep ? ex2(fmaf(s[c], sl2, -st[c])) : 0.f;
+            pv[e] = pr;
+            dv[e] = pr * (dp[c] - st[BQ + c]) * scale;
+          }
+          pw[j / 2] = pack_bf16(pv[0], pv[1]);
+          dw[j / 2] = pack_bf16(dv[0], dv[1]);
+        }
+        *reinterpret_cast<uint4*>(prow + sw128_offset(r, c8)) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+        *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, c8)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars.ds_full[b]);
+      ++it;
+    }
+    // ---------------------------------------------------------- dV epilogue
+    float acc[D];
+    if (it > 0) {
+      mbar_wait(&bars.dkv_full, 0);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(tmem + lane_base + 256 + c * 32, rr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __uint_as_float(rr[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[j] = 0.f;
+    }
+    if (key_ok) {
+      float* dst = p.dv + ((size_t)hk * p.Tk + key) * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 4) {
+        float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        if (p.accumulate_kv) {
+          const float4 o = *reinterpret_cast<const float4*>(dst + c);
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        *reinterpret_cast<float4*>(dst + c) = v;
+      }
+    }
+  } else if (warp >= 8) {
+    // -------------------------------------------------------------- WG-B: dQ drain
+    const int wq = warp % 4;
+    const int d = wq * 32 + lane;  // TMEM lane of dQ^T == feature index
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    int it = 0;
+    for (int i = 0; i < n_iter_max; ++i) {
+      const int g = i / nqt, qt = i % nqt;
+      if (!live(qt)) continue;
+      const int h = hk * p.G + g;
+      const int b = it & 1;
+      mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t v0[32], v1[32];
+      tmem_ld32(tmem + lane_base + b * 128, v0);
+      tmem_ld32(tmem + lane_base + b * 128 + 32, v1);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars.dq_empty[b]);
+      float* dst = p.dq_acc + ((size_t)h * p.Tq + qt * BQ) * D + d;
+      const int rows = min(BQ, p.Tq - qt * BQ);
+      if (rows == BQ) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) atomicAdd(dst + (size_t)c * D, __uint_as_float(v0[c]));
+#pragma unroll
+        for (int c = 0; c < 32; ++c) atomicAdd(dst + (size_t)(c + 32) * D, __uint_as_float(v1[c]));
+      } else {
+        for (int c = 0; c < 32; ++c)
+          if (c < rows) atomicAdd(dst + (size_t)c * D, __uint_as_float(v0[c]));
+        for (int c = 0; c < 32; ++c)
+          if (c + 32 < rows) atomicAdd(dst + (size_t)(c + 32) * D, __uint_as_float(v1[c]));
+      }
+      ++it;
+    }
+    // ---------------------------------------------------------- dK epilogue
+    const int r = d;
+    const int key = key0 + r;
+    float acc[D];
+    if (it > 0) {
+      mbar_wait(&bars.dkv_full, 0);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(tmem + lane_base + 384 + c * 32, rr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __uint_as_float(rr[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[j] = 0.f;
+    }
+    if (key < p.Tk) {
+      float* dst = p.dk + ((size_t)hk * p.Tk + key) * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 4) {
+        float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        if (p.accumulate_kv) {
+          const float4 o = *reinterpret_cast<const float4*>(dst + c);
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        *reinterpret_cast<float4*>(dst + c) = v;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
+  if (head_dim != 128) return cudaErrorInvalidValue;
+  if (p.Tk <= 0 || p.Hkv <= 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd::kBytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid((p.Tk + bwd::BK - 1) / bwd::BK, p.Hkv);
+  fa_bwd_kernel<<<grid, bwd::kThreads, bwd::kBytes, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace a2d

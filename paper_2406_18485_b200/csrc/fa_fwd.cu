@@ -1,0 +1,385 @@
+// Chunk flash-attention forward for sm_100a (K1) with the ring-step LSE merge
+// fused into the epilogue (K2).
+//
+// Computes, for one Q chunk against one KV chunk (one ring step of
+// run_double_ring, ref ring.py:64-79 / oracle.py:97-124):
+//   blk.out = softmax(mask(Q K^T / sqrt(d))) V,  blk.lse = natural-log LSE
+// and either writes blk (mode 0) or folds it into a running fp32 accumulator
+// exactly like block_update (mode 1).  The causal mask compares the carried
+// original token positions (ref oracle.py:73-75), so zig-zag chunks need no
+// special casing: tiles whose keys all lie after every query are skipped,
+// tiles entirely in the past run unmasked, only straddling tiles mask.
+//
+// Structure (one CTA = 2 query tiles of 128 rows of one head, 12 warps):
+//   warp 0      TMA producer: Q once, then K/V tiles through 2-stage rings
+//   warp 1      MMA issuer (one thread): S_t = Q_t K^T into TMEM, O_t += P_t V
+//   warp 2      TMEM allocator
+//   warps 4-7   softmax for query tile 0 (thread = row = TMEM lane)
+//   warps 8-11  softmax for query tile 1
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D);
+// P_t (bf16) is written over the first 64 columns of S_t and consumed by a
+// TMEM-operand (TS) UMMA. The two softmax groups ping-pong so the tensor core
+// runs one tile's GEMMs while the other tile's softmax runs.
+// Rescaling of O is lazy: the running max only moves when a row max grows by
+// more than 2^8, so O is touched on a handful of tiles per row at most.
+#include "sm100.cuh"
+#include "kernels.h"
+
+namespace a2d {
+
+namespace fwd {
+constexpr int BM = 128, BN = 128;
+constexpr int kThreads = 384;
+constexpr int KST = 2, VST = 2;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+}  // namespace fwd
+
+template <int D>
+struct FwdSmem {
+  static constexpr int kTileBytes = 128 * D * 2;  // one 128-row bf16 tile
+  static constexpr int kQ = 0;
+  static constexpr int kK = kQ + 2 * kTileBytes;
+  static constexpr int kV = kK + fwd::KST * kTileBytes;
+  static constexpr int kEnd = kV + fwd::VST * kTileBytes;
+  static constexpr int kBytes = kEnd + 1024;  // + alignment slack
+};
+
+struct FwdBars {
+  uint64_t q_full;
+  uint64_t k_full[fwd::KST], k_empty[fwd::KST];
+  uint64_t v_full[fwd::VST], v_empty[fwd::VST];
+  uint64_t s_full[2], p_full[2], o_full[2];
+  uint32_t tmem_base;
+};
+
+// Tile classification against one query tile's position range.
+__device__ __forceinline__ bool tile_live(int2 kb, int qmax, bool causal) {
+  return kb.x <= kb.y && (!causal || kb.x <= qmax);
+}
+
+template <int D>
+__global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_constant__ FwdParams p) {
+  using namespace fwd;
+  using L = FwdSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ FwdBars bars;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nqb = (p.Tq + 2 * BM - 1) / (2 * BM);
+  const int qb = nqb - 1 - (int)blockIdx.x;  // heaviest (latest) query blocks first
+  const int h = blockIdx.y;
+  const int hk = h / p.G;
+  const int q0 = qb * 2 * BM;
+  const int nkt = (p.Tk + BN - 1) / BN;
+
+  // query-tile position ranges (tiles beyond Tq have min > max)
+  const int nqt = (p.Tq + BM - 1) / BM;
+  int2 qr0 = (2 * qb < nqt) ? p.q_bounds[2 * qb] : make_int2(1, 0);
+  int2 qr1 = (2 * qb + 1 < nqt) ? p.q_bounds[2 * qb + 1] : make_int2(1, 0);
+  const int qmax_cta = max(qr0.x <= qr0.y ? qr0.y : INT_MIN, qr1.x <= qr1.y ? qr1.y : INT_MIN);
+  const bool causal = p.causal != 0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.q_full, 1);
+    for (int i = 0; i < KST; ++i) { mbar_init(&bars.k_full[i], 1); mbar_init(&bars.k_empty[i], 1); }
+    for (int i = 0; i < VST; ++i) { mbar_init(&bars.v_full[i], 1); mbar_init(&bars.v_empty[i], 1); }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bars.s_full[t], 1);
+      mbar_init(&bars.p_full[t], 128);
+      mbar_init(&bars.o_full[t], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars.tmem_base);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tm_q);
+    tma_prefetch(&p.tm_k);
+    tma_prefetch(&p.tm_v);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+
+  // number of live KV tiles for the CTA (same loop in every role)
+  auto live = [&](int j) { return tile_live(p.k_bounds[j], qmax_cta, causal); };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      mbar_expect_tx(&bars.q_full, 2 * L::kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(smem + L::kQ + t * L::kTileBytes + c * 16384, &p.tm_q, &bars.q_full, c * 64,
+                      q0 + t * BM, h);
+      int it = 0;
+      for (int j = 0; j < nkt; ++j) {
+        if (!live(j)) continue;
+        const int ks = it % KST, kph = (it / KST) & 1;
+        mbar_wait(&bars.k_empty[ks], kph ^ 1);
+        mbar_expect_tx(&bars.k_full[ks], L::kTileBytes);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(smem + L::kK + ks * L::kTileBytes + c * 16384, &p.tm_k, &bars.k_full[ks], c * 64,
+                      j * BN, hk);
+        const int vs = it % VST, vph = (it / VST) & 1;
+        mbar_wait(&bars.v_empty[vs], vph ^ 1);
+        mbar_expect_tx(&bars.v_full[vs], L::kTileBytes);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(smem + L::kV + vs * L::kTileBytes + c * 16384, &p.tm_v, &bars.v_full[vs], c * 64,
+                      j * BN, hk);
+        ++it;
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int n = 0;
+      for (int j = 0; j < nkt; ++j) n += live(j) ? 1 : 0;
+      constexpr uint32_t id_qk = idesc_bf16(BM, BN, false, false);
+      constexpr uint32_t id_pv = idesc_bf16(BM, D, false, true);
+      const uint32_t sq = smem_u32(smem + L::kQ), sk = smem_u32(smem + L::kK), sv = smem_u32(smem + L::kV);
+      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      auto issue_qk = [&](int t, int ks) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
+          umma_ss(tS[t], sdesc_sw128(sq + t * L::kTileBytes + off, 16, 1024),
+                  sdesc_sw128(sk + ks * L::kTileBytes + off, 16, 1024), id_qk, k > 0);
+        }
+      };
+      auto issue_pv = [&](int t, int vs, bool acc) {
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k)
+          umma_ts(tO[t], tS[t] + k * 8, sdesc_sw128(sv + vs * L::kTileBytes + k * 2048, 16384, 1024), id_pv,
+                  (acc || k > 0) ? 1u : 0u);
+      };
+      if (n > 0) {
+        mbar_wait(&bars.q_full, 0);
+        mbar_wait(&bars.k_full[0], 0);
+        tc_fence_after();
+        issue_qk(0, 0);
+        umma_commit(&bars.s_full[0]);
+        issue_qk(1, 0);
+        umma_commit(&bars.s_full[1]);
+        umma_commit(&bars.k_empty[0]);
+        for (int it = 0; it < n; ++it) {
+          const int vs = it % VST;
+          mbar_wait(&bars.v_full[vs], (it / VST) & 1);
+          const bool more = it + 1 < n;
+          const int ks1 = (it + 1) % KST;
+          mbar_wait(&bars.p_full[0], it & 1);
+          tc_fence_after();
+          issue_pv(0, vs, it > 0);
+          if (more) {
+            mbar_wait(&bars.k_full[ks1], ((it + 1) / KST) & 1);
+            tc_fence_after();
+            issue_qk(0, ks1);
+            umma_commit(&bars.s_full[0]);
+          } else {
+            umma_commit(&bars.o_full[0]);
+          }
+          mbar_wait(&bars.p_full[1], it & 1);
+          tc_fence_after();
+          issue_pv(1, vs, it > 0);
+          umma_commit(&bars.v_empty[vs]);
+          if (more) {
+            issue_qk(1, ks1);
+            umma_commit(&bars.s_full[1]);
+            umma_commit(&bars.k_empty[ks1]);
+          } else {
+            umma_commit(&bars.o_full[1]);
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax
+    const int t = (warp - 4) / 4;          // query tile of this warpgroup
+    const int wq = warp % 4;               // TMEM lane quarter
+    const int row_in_tile = wq * 32 + lane;
+    const int row = q0 + t * BM + row_in_tile;
+    const bool row_ok = row < p.Tq;
+    const int qpos = row_ok ? p.q_pos[row] : INT_MIN;
+    const int2 qr = t == 0 ? qr0 : qr1;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const uint32_t tS = tmem + lane_base + t * 128;
+    const uint32_t tO = tmem + lane_base + 256 + t * 128;
+    const float sl2 = p.scale_log2;
+
+    float m_used = -INFINITY;  // running max, log2 units (scaled)
+    float l_sum = 0.f;
+    int it = 0;
+    for (int j = 0; j < nkt; ++j) {
+      const int2 kb = p.k_bounds[j];
+      if (!tile_live(kb, qmax_cta, causal)) continue;
+      // tile status for this query tile: full (no mask), or masked
+      const bool tail = (j + 1) * BN > p.Tk;
+      const bool dead = causal && (qr.x > qr.y || kb.x > qr.y);
+      const bool full = !tail && !dead && (!causal || kb.y <= qr.x);
+
+      mbar_wait(&bars.s_full[t], it & 1);
+      tc_fence_after();
+      float s[BN];
+      {
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          tmem_ld32(tS + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+        }
+      }
+      if (!full) {
+        const int* kp = p.k_pos + j * BN;
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          const int col = j * BN + c;
+          bool keep = col < p.Tk && !dead;
+          if (keep && causal) keep = __ldg(kp + c) <= qpos;
+          if (!keep) s[c] = -INFINITY;
+        }
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < BN; ++c) mx = fmaxf(mx, s[c]);
+      const float m_tile = mx * sl2;  // -inf stays -inf (sl2 > 0)
+      float alpha = 1.f;
+      bool rescale = false;
+      if (m_tile > m_used + kRescaleThreshold) {
+        if (m_used != -INFINITY) { alpha = ex2(m_used - m_tile); rescale = true; }
+        m_used = m_tile;
+        l_sum *= alpha;
+      }
+      const float neg_m = m_used == -INFINITY ? 0.f : -m_used;
+      float part[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[BN / 2];
+#pragma unroll
+      for (int c = 0; c < BN; c += 2) {
+        const float a = ex2(fmaf(s[c], sl2, neg_m));
+        const float b = ex2(fmaf(s[c + 1], sl2, neg_m));
+        part[(c / 2) & 3] += a + b;
+        pk[c / 2] = pack_bf16(a, b);
+      }
+      l_sum += (part[0] + part[1]) + (part[2] + part[3]);
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) {
+        uint32_t r[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = pk[c * 32 + i];
+        tmem_st32(tS + c * 32, r);
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+        // O (this tile's previous PV) is complete: s_full's commit tracks it.
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st32(tO + c * 32, r);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars.p_full[t]);
+      ++it;
+    }
+
+    // ---------------------------------------------------------- epilogue
+    float o[D];
+    if (it > 0) {
+      mbar_wait(&bars.o_full[t], 0);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tO + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[c * 32 + i] = __uint_as_float(r[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < D; ++i) o[i] = 0.f;
+    }
+    if (row_ok) {
+      const bool alive = l_sum > 0.f;
+      const float inv = alive ? 1.f / l_sum : 0.f;
+      const float lse_blk = alive ? (m_used + __log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+      const size_t lrow = (size_t)h * p.Tq + row;
+      float wa = 0.f, wb = inv, lse_new = lse_blk;
+      if (p.merge) {
+        const float la = p.lse[lrow];
+        const float mx2 = fmaxf(la, lse_blk);
+        if (mx2 == -INFINITY) {
+          lse_new = -INFINITY;
+          wa = 0.f;
+          wb = 0.f;
+        } else {
+          const float ea = la == -INFINITY ? 0.f : __expf(la - mx2);
+          const float eb = lse_blk == -INFINITY ? 0.f : __expf(lse_blk - mx2);
+          const float z = ea + eb;
+          lse_new = mx2 + __logf(z);
+          wa = ea / z;
+          wb = eb / z * inv;
+        }
+      }
+      p.lse[lrow] = lse_new;
+      float* acc = p.acc_o ? p.acc_o + ((size_t)h * p.Tq + row) * D : nullptr;
+      __nv_bfloat16* out = p.out ? p.out + (size_t)h * p.out_stride_h + (size_t)row * p.out_stride_t : nullptr;
+#pragma unroll
+      for (int c = 0; c < D; c += 8) {
+        float v[8];
+        if (p.merge) {
+          const float4 a0 = *reinterpret_cast<const float4*>(acc + c);
+          const float4 a1 = *reinterpret_cast<const float4*>(acc + c + 4);
+          v[0] = a0.x * wa + o[c] * wb; v[1] = a0.y * wa + o[c + 1] * wb;
+          v[2] = a0.z * wa + o[c + 2] * wb; v[3] = a0.w * wa + o[c + 3] * wb;
+          v[4] = a1.x * wa + o[c + 4] * wb; v[5] = a1.y * wa + o[c + 5] * wb;
+          v[6] = a1.z * wa + o[c + 6] * wb; v[7] = a1.w * wa + o[c + 7] * wb;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = o[c + i] * wb;
+        }
+        if (acc) {
+          *reinterpret_cast<float4*>(acc + c) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(acc + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        }
+        if (out) {
+          uint4 u;
+          u.x = pack_bf16(v[0], v[1]); u.y = pack_bf16(v[2], v[3]);
+          u.z = pack_bf16(v[4], v[5]); u.w = pack_bf16(v[6], v[7]);
+          *reinterpret_cast<uint4*>(out + c) = u;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+template <int D>
+static cudaError_t launch_fwd_d(const FwdParams& p, cudaStream_t s) {
+  const int smem = FwdSmem<D>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int nqb = (p.Tq + 255) / 256;
+  dim3 grid(nqb, p.H);
+  fa_fwd_kernel<D><<<grid, fwd::kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s) {
+  if (p.Tq <= 0 || p.H <= 0) return cudaSuccess;
+  if (head_dim == 128) return launch_fwd_d<128>(p, s);
+  if (head_dim == 64) return launch_fwd_d<64>(p, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace a2d

@@ -1,0 +1,177 @@
+"""torch-facing wrappers over the C ABI (device memory, streams, padding).
+
+Every function here launches CUDA work through ``libattn2d_sm100.so`` on the
+current torch stream; none has a CPU path. Tensor layout is head-major
+``[H][T][D]`` (the reference's DenseTensor.values, oracle.py:15-34).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+
+BF16 = torch.bfloat16
+FWD_DIMS = (64, 128)
+BWD_DIM = 128
+
+
+def _ptr(t):
+    return None if t is None else ctypes_ptr(t)
+
+
+def ctypes_ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _check_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("tensor must live on a CUDA device")
+
+
+def fwd_dim(d: int) -> int:
+    """Kernel head dim for a true head dim d (zero padding, exact)."""
+    if d <= 64:
+        return 64
+    if d <= 128:
+        return 128
+    raise ValueError(f"head_dim {d} > 128 not supported")
+
+
+def pad_dim(x: torch.Tensor, dk: int) -> torch.Tensor:
+    """bf16, contiguous, last dim zero-padded to dk (QK^T and PV unchanged)."""
+    x = x.to(BF16)
+    if x.shape[-1] != dk:
+        x = torch.nn.functional.pad(x, (0, dk - x.shape[-1]))
+    return x.contiguous()
+
+
+def tile_bounds(pos: torch.Tensor, tile: int) -> torch.Tensor:
+    """[ceil(T/tile), 2] int32 (min, max) of positions per tile."""
+    _check_cuda(pos)
+    pos = pos.to(torch.int32).contiguous()
+    n = (pos.numel() + tile - 1) // tile
+    out = torch.empty((max(n, 1), 2), dtype=torch.int32, device=pos.device)
+    _lib.call("a2d_tile_bounds", pos.data_ptr(), pos.numel(), tile, out.data_ptr(), _stream())
+    return out
+
+
+class ChunkPlan:
+    """Positions + tile bounds of one chunk, cached for reuse across steps."""
+
+    def __init__(self, pos: torch.Tensor):
+        self.pos = pos.to(torch.int32).contiguous()
+        self.b128 = tile_bounds(self.pos, 128)
+        self.b64 = tile_bounds(self.pos, 64)
+
+    @property
+    def T(self) -> int:
+        return self.pos.numel()
+
+
+def fwd_chunk(q, k, v, qp: ChunkPlan, kp: ChunkPlan, causal: bool, scale: float,
+              lse: torch.Tensor, acc_o: torch.Tensor | None = None,
+              out: torch.Tensor | None = None, merge: bool = False) -> None:
+    """One ring step forward (K1 + fused K2). q/k/v bf16 [H|Hkv][T][D], D in {64,128}."""
+    _check_cuda(q, k, v)
+    H, Tq, D = q.shape
+    Hkv, Tk, _ = k.shape
+    if D not in FWD_DIMS:
+        raise ValueError(f"kernel head dim must be 64 or 128, got {D}")
+    for t in (q, k, v):
+        if t.dtype != BF16 or not t.is_contiguous():
+            raise ValueError("q/k/v must be contiguous bf16")
+    if k.shape != v.shape:
+        raise ValueError("K and V shapes differ")
+    _lib.call("a2d_fa_fwd_chunk", q.data_ptr(), k.data_ptr(), v.data_ptr(), qp.pos.data_ptr(),
+              kp.pos.data_ptr(), qp.b128.data_ptr(), kp.b128.data_ptr(), H, Hkv, Tq, Tk, D,
+              int(causal), float(scale), int(merge), lse.data_ptr(),
+              None if acc_o is None else acc_o.data_ptr(),
+              None if out is None else out.data_ptr(), _stream())
+
+
+def bwd_preprocess(o: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor):
+    """(lse2, delta) fp32 [H][Tq_pad64]."""
+    H, Tq, D = o.shape
+    tp = (Tq + 63) // 64 * 64
+    lse2 = torch.empty((H, tp), dtype=torch.float32, device=o.device)
+    delta = torch.empty((H, tp), dtype=torch.float32, device=o.device)
+    _lib.call("a2d_bwd_preprocess", o.data_ptr(), dout.data_ptr(), lse.data_ptr(), H, Tq, D,
+              lse2.data_ptr(), delta.data_ptr(), _stream())
+    return lse2, delta
+
+
+def bwd_chunk(q, k, v, dout, qp: ChunkPlan, kp: ChunkPlan, lse2, delta, dq_acc, dk, dv,
+              accumulate_kv: bool, causal: bool, scale: float) -> None:
+    """One ring step backward (K3). q/k/v/dout bf16 D=128; dq_acc/dk/dv fp32."""
+    H, Tq, D = q.shape
+    Hkv, Tk, _ = k.shape
+    if D != BWD_DIM:
+        raise ValueError("backward kernel head dim must be 128")
+    _lib.call("a2d_fa_bwd_chunk", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
+              qp.pos.data_ptr(), kp.pos.data_ptr(), qp.b64.data_ptr(), kp.b128.data_ptr(),
+              lse2.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+              int(accumulate_kv), H, Hkv, Tq, Tk, D, int(causal), float(scale), _stream())
+
+
+def merge_(acc_o, acc_lse, blk_o, blk_lse) -> None:
+    """In-place block_update of fp32 (acc_o, acc_lse) with (blk_o, blk_lse)."""
+    d = acc_o.shape[-1]
+    rows = acc_o.numel() // d
+    _lib.call("a2d_merge", acc_o.data_ptr(), acc_lse.data_ptr(), blk_o.contiguous().float().data_ptr()
+              if blk_o.dtype != torch.float32 else blk_o.data_ptr(), blk_lse.data_ptr(), rows, d, _stream())
+
+
+def permute_blocks(src: torch.Tensor, A: int, B: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[b][a] = src[a][b] with src viewed as [A][B][blk] (bit-exact byte move)."""
+    src = src.contiguous()
+    if out is None:
+        out = torch.empty_like(src)
+    blk = src.numel() * src.element_size() // max(A * B, 1)
+    _lib.call("a2d_permute_blocks", src.data_ptr(), out.data_ptr(), A, B, blk, _stream())
+    return out
+
+
+def gather_blocks(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """out[i] = src[index[i]] over leading-dim blocks."""
+    blk = src[0].numel() * src.element_size()
+    idx = index.to(device=src.device, dtype=torch.int32).contiguous()
+    _lib.call("a2d_gather_blocks", src.data_ptr(), out.data_ptr(), idx.data_ptr(), idx.numel(), blk, _stream())
+    return out
+
+
+def sum_replicas(src: torch.Tensor, rep: int) -> torch.Tensor:
+    """[H*rep, ...] fp32 -> [H, ...] summing consecutive copies."""
+    heads = src.shape[0] // rep
+    out = torch.empty((heads,) + tuple(src.shape[1:]), dtype=torch.float32, device=src.device)
+    _lib.call("a2d_sum_replicas_f32", src.data_ptr(), out.data_ptr(), heads, rep, src[0].numel(), _stream())
+    return out
+
+
+def to_bf16(src: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(src.shape, dtype=BF16, device=src.device)
+    _lib.call("a2d_f32_to_bf16", src.data_ptr(), out.data_ptr(), src.numel(), _stream())
+    return out
+
+
+def add_(dst: torch.Tensor, src: torch.Tensor) -> None:
+    _lib.call("a2d_add_f32", dst.data_ptr(), src.data_ptr(), dst.numel(), _stream())
+
+
+def selftest_umma(a, b, v, at) -> torch.Tensor:
+    c = torch.empty((4, 128, 128), dtype=torch.float32, device=a.device)
+    _lib.call("a2d_selftest_umma", a.data_ptr(), b.data_ptr(), v.data_ptr(), at.data_ptr(), c.data_ptr(),
+              _stream())
+    return c
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

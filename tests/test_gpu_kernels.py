@@ -1,0 +1,192 @@
+"""Single-GPU parity of the sm_100a kernels against the CPU oracle and the
+reference's golden vectors. Tolerances (BASELINE.json north star): bf16
+kernels vs the f64 oracle, max-abs <= 2e-2 and rel-L2 <= 1e-2 (O, LSE, dQ, dK,
+dV); permutations bit-exact."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import bf16_bits_to_f64, golden
+from oracle import attn2d_oracle as orc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-2
+REL_L2 = 1e-2
+
+
+def close(name, got, ref, max_abs=MAX_ABS, rel=REL_L2):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert got.shape == ref.shape, (name, got.shape, ref.shape)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(got), fin), f"{name}: finiteness pattern differs"
+    if not fin.any():
+        return
+    d = np.abs(got[fin] - ref[fin])
+    ma = float(d.max())
+    rl = float(np.linalg.norm(d) / max(np.linalg.norm(ref[fin]), 1e-30))
+    assert ma <= max_abs and rl <= rel, f"{name}: max-abs {ma:.3e}, rel-L2 {rl:.3e}"
+
+
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def t_bf16(bits, device):
+    x = torch.from_numpy(np.asarray(bits, np.uint16).view(np.int16).copy())
+    return x.view(torch.bfloat16).to(device)
+
+
+def bf16_round(x):
+    return torch.from_numpy(np.asarray(x, np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def test_umma_selftest():
+    from paper_2406_18485_b200 import kernels as K
+    d = dev()
+    g = torch.Generator().manual_seed(0)
+    a, b, v, at = (torch.randn(128, 128, generator=g).to(torch.bfloat16).to(d) for _ in range(4))
+    c = K.selftest_umma(a, b, v, at).cpu().double()
+    A, B, V, AT = (x.double().cpu() for x in (a, b, v, at))
+    refs = [A @ B.T, A @ V, AT.T @ B.T, A @ V]
+    for i, r in enumerate(refs):
+        err = (c[i] - r).abs().max().item()
+        assert err < 1e-2 * max(1.0, r.abs().max().item() / 10), f"case {i}: max err {err}"
+
+
+def _fwd(q, k, v, q_pos, k_pos, causal, device, scale=None):
+    from paper_2406_18485_b200 import kernels as K
+    d = q.shape[-1]
+    dk = K.fwd_dim(d)
+    qt, kt, vt = (K.pad_dim(torch.from_numpy(np.asarray(x, np.float32)).to(device), dk) for x in (q, k, v))
+    qp = K.ChunkPlan(torch.as_tensor(q_pos, dtype=torch.int32, device=device))
+    kp = K.ChunkPlan(torch.as_tensor(k_pos, dtype=torch.int32, device=device))
+    H, T = q.shape[0], q.shape[1]
+    lse = torch.empty((H, T), dtype=torch.float32, device=device)
+    acc = torch.empty((H, T, dk), dtype=torch.float32, device=device)
+    out = torch.empty((H, T, dk), dtype=torch.bfloat16, device=device)
+    K.fwd_chunk(qt, kt, vt, qp, kp, causal, scale or 1.0 / math.sqrt(d), lse, acc, out)
+    torch.cuda.synchronize()
+    return acc[..., :d].cpu().numpy(), lse.cpu().numpy(), out[..., :d].float().cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["mha_d128_s256_c", "gqa_d128_s384_c", "mha_d64_s256_n", "gqa_d128_s200_n"])
+def test_fwd_chunk_golden(name):
+    d = dev()
+    g = golden(f"gpu_{name}.npz")
+    q, k, v = (bf16_bits_to_f64(g[n]) for n in "qkv")
+    pos = np.arange(q.shape[1])
+    o, lse, ob = _fwd(q, k, v, pos, pos, bool(g["causal"]), d)
+    close(f"{name} O", o, g["out"])
+    close(f"{name} O(bf16)", ob, g["out"])
+    close(f"{name} LSE", lse, g["lse"])
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("shape", [(4, 4, 1024, 128), (8, 2, 640, 128), (2, 1, 300, 64), (2, 2, 7, 128)])
+def test_fwd_chunk_oracle(shape, causal):
+    d = dev()
+    H, Hkv, T, D = shape
+    q, k, v = (bf16_round(x) for x in orc.philox_qkv(31, H, Hkv, T, D))
+    pos = np.arange(T)
+    o, lse, _ = _fwd(q, k, v, pos, pos, causal, d)
+    ro, rl = orc.attention(q, k, v, pos, pos, causal)
+    close("O", o, ro)
+    close("LSE", lse, rl)
+
+
+@pytest.mark.parametrize("d_cp", [2, 4])
+def test_fwd_zigzag_steps_and_merge(d_cp):
+    """Every (Q chunk j, KV chunk s) pair of a zig-zag ring, folded with the
+    fused merge, equals full attention (ref run_double_ring)."""
+    from paper_2406_18485_b200 import kernels as K
+    d = dev()
+    H, S, D = 2, 1024, 128
+    q, k, v = (bf16_round(x) for x in orc.philox_qkv(5, H, H, S, D))
+    perm, _ = orc.zigzag(S, d_cp)
+    C = S // d_cp
+    ro, rl = orc.attention(q, k, v, np.arange(S), np.arange(S), True)
+    for j in range(d_cp):
+        qpos = perm[j * C:(j + 1) * C]
+        qt = K.pad_dim(torch.from_numpy(q[:, qpos].astype(np.float32)).to(d), 128)
+        qp = K.ChunkPlan(torch.as_tensor(qpos, dtype=torch.int32, device=d))
+        lse = torch.empty((H, C), dtype=torch.float32, device=d)
+        acc = torch.empty((H, C, 128), dtype=torch.float32, device=d)
+        for step, s in enumerate(orc.ring_sources(d_cp, d_cp)[j]):
+            kpos = perm[s * C:(s + 1) * C]
+            kt = K.pad_dim(torch.from_numpy(k[:, kpos].astype(np.float32)).to(d), 128)
+            vt = K.pad_dim(torch.from_numpy(v[:, kpos].astype(np.float32)).to(d), 128)
+            kp = K.ChunkPlan(torch.as_tensor(kpos, dtype=torch.int32, device=d))
+            K.fwd_chunk(qt, kt, vt, qp, kp, True, 1 / math.sqrt(D), lse, acc, None, merge=step > 0)
+        torch.cuda.synchronize()
+        close(f"rank {j} O", acc.cpu().numpy(), ro[:, qpos])
+        close(f"rank {j} LSE", lse.cpu().numpy(), rl[:, qpos])
+
+
+def _bwd(q, k, v, do, q_pos, k_pos, causal, device):
+    from paper_2406_18485_b200 import kernels as K
+    D = q.shape[-1]
+    fd = K.fwd_dim(D)
+    H, T = q.shape[0], q.shape[1]
+    Hkv, Tk = k.shape[0], k.shape[1]
+    t = lambda x, dd: K.pad_dim(torch.from_numpy(np.asarray(x, np.float32)).to(device), dd)  # noqa: E731
+    qp = K.ChunkPlan(torch.as_tensor(q_pos, dtype=torch.int32, device=device))
+    kp = K.ChunkPlan(torch.as_tensor(k_pos, dtype=torch.int32, device=device))
+    scale = 1 / math.sqrt(D)
+    lse = torch.empty((H, T), dtype=torch.float32, device=device)
+    out = torch.empty((H, T, fd), dtype=torch.bfloat16, device=device)
+    K.fwd_chunk(t(q, fd), t(k, fd), t(v, fd), qp, kp, causal, scale, lse, None, out)
+    dot = t(do, fd)
+    lse2, delta = K.bwd_preprocess(out, dot, lse)
+    dq = torch.zeros((H, T, 128), dtype=torch.float32, device=device)
+    dk = torch.empty((Hkv, Tk, 128), dtype=torch.float32, device=device)
+    dv = torch.empty((Hkv, Tk, 128), dtype=torch.float32, device=device)
+    K.bwd_chunk(t(q, 128), t(k, 128), t(v, 128), t(do, 128), qp, kp, lse2, delta, dq, dk, dv, False,
+                causal, scale)
+    torch.cuda.synchronize()
+    return (dq[..., :D].cpu().numpy(), dk[..., :D].cpu().numpy(), dv[..., :D].cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["mha_d128_s256_c", "gqa_d128_s384_c", "mha_d64_s256_n", "gqa_d128_s200_n"])
+def test_bwd_chunk_golden(name):
+    d = dev()
+    g = golden(f"gpu_{name}.npz")
+    q, k, v, do = (bf16_bits_to_f64(g[n]) for n in ("q", "k", "v", "do"))
+    pos = np.arange(q.shape[1])
+    dq, dk, dv = _bwd(q, k, v, do, pos, pos, bool(g["causal"]), d)
+    close(f"{name} dQ", dq, g["dq"])
+    close(f"{name} dK", dk, g["dk"])
+    close(f"{name} dV", dv, g["dv"])
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("shape", [(4, 2, 768, 128), (2, 2, 130, 128)])
+def test_bwd_chunk_oracle(shape, causal):
+    d = dev()
+    H, Hkv, T, D = shape
+    q, k, v = (bf16_round(x) for x in orc.philox_qkv(77, H, Hkv, T, D))
+    do = bf16_round(np.random.Generator(np.random.Philox(78)).standard_normal(q.shape))
+    pos = np.arange(T)
+    dq, dk, dv = _bwd(q, k, v, do, pos, pos, causal, d)
+    rq, rk, rv = orc.attention_grads(q, k, v, do, pos, pos, causal)
+    close("dQ", dq, rq)
+    close("dK", dk, rk)
+    close("dV", dv, rv)
+
+
+def test_permute_and_gather_bit_exact():
+    from paper_2406_18485_b200 import kernels as K
+    d = dev()
+    x = torch.randint(-2**15, 2**15, (4, 3, 40, 16), dtype=torch.int16, device=d).view(torch.bfloat16)
+    y = K.permute_blocks(x, 4, 3)
+    assert torch.equal(y.view(torch.int16), x.view(torch.int16).permute(1, 0, 2, 3).contiguous())
+    idx = torch.tensor([2, 0, 0, 1, 3, 3], dtype=torch.int32, device=d)
+    out = torch.empty((6, 3, 40, 16), dtype=torch.bfloat16, device=d)
+    K.gather_blocks(x, idx, out)
+    assert torch.equal(out.view(torch.int16), x.view(torch.int16)[idx.long()])
