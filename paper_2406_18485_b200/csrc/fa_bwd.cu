@@ -19,8 +19,10 @@
 //   dK  += dS^T Q                                  TMEM [384,512)
 // P^T and dS^T go through shared memory in the SW128 K-major layout; the same
 // bytes are the MN-major B operand of dQ^T, so one copy serves both GEMMs.
-// Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 "WG-A" (P, dS), 8-11 "WG-B"
-// (drain dQ^T with fp32 reductions into dq_acc, overlapping dV/dK GEMMs).
+// Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 two compute warpgroups that
+// split every 64-query iteration in halves: P and dS for their 32 query
+// columns, then the matching half of dQ^T drained with fp32 reductions into
+// dq_acc while the tensor core runs dV/dK.
 #include "sm100.cuh"
 #include "kernels.h"
 
@@ -63,7 +65,7 @@ A2D_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_constant__ BwdParams p) {
   using namespace bwd;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   __shared__ BwdBars bars;
 
   const int warp = warp_id(), lane = lane_id();
@@ -88,9 +90,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     for (int i = 0; i < QST; ++i) { mbar_init(&bars.qdo_full[i], 1); mbar_init(&bars.qdo_empty[i], 1); }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars.s_full[b], 1);
-      mbar_init(&bars.ds_full[b], 128);
+      mbar_init(&bars.ds_full[b], 256);
       mbar_init(&bars.dq_full[b], 1);
-      mbar_init(&bars.dq_empty[b], 128);
+      mbar_init(&bars.dq_empty[b], 256);
       mbar_init(&bars.pds_free[b], 1);
     }
     mbar_init(&bars.dkv_full, 1);
@@ -195,163 +197,125 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         umma_commit(&bars.dkv_full);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // -------------------------------------------------------------- WG-A: P, dS
+  } else if (warp >= 4) {
+    // ------------------------------------------------ compute warpgroups
+    // Both warpgroups cover all 128 key rows (TMEM lanes); warpgroup hq owns
+    // query columns [32*hq, 32*hq+32) of every iteration, for P/dS and for
+    // the dQ^T drain (where the TMEM lane is the feature index d).
+    const int hq = (warp - 4) / 4;
     const int wq = warp % 4;
-    const int r = wq * 32 + lane;  // key row in tile == TMEM lane
+    const int r = wq * 32 + lane;
     const int key = key0 + r;
     const bool key_ok = key < p.Tk;
     const int kpos = key_ok ? p.k_pos[key] : INT_MAX;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const float sl2 = p.scale_log2, scale = p.scale;
+    const int c0 = hq * 32;
     int it = 0;
     for (int i = 0; i < n_iter_max; ++i) {
-      const int qt = i % nqt;
-      if (!live(qt)) continue;
+      const int g = i / nqt, qt = i % nqt;
       const int2 qb = p.q_bounds[qt];
+      if (!(qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y))) continue;
       const bool full = !causal || kb.y <= qb.x;
+      const int h = hk * p.G + g;
       const int b = it & 1, qs = it % QST;
-      mbar_wait(&bars.qdo_full[qs], (it / QST) & 1);  // stats landed (TMA done)
-      mbar_wait(&bars.s_full[b], (it >> 1) & 1);
-      tc_fence_after();
-      float s[BQ], dp[BQ];
-      {
-        uint32_t rr[32];
+      int qpos[32];
+      if (!full) {
 #pragma unroll
-        for (int c = 0; c < BQ / 32; ++c) {
-          tmem_ld32(tmem + lane_base + b * 128 + c * 32, rr);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(rr[j]);
-          tmem_ld32(tmem + lane_base + b * 128 + 64 + c * 32, rr);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) dp[c * 32 + j] = __uint_as_float(rr[j]);
+        for (int c = 0; c < 32; ++c) {
+          const int q = qt * BQ + c0 + c;
+          qpos[c] = q < p.Tq ? __ldg(p.q_pos + q) : INT_MIN;
         }
       }
-      const float* st = reinterpret_cast<const float*>(smem + kStats) + qs * 2 * BQ;
+      mbar_wait(&bars.qdo_full[qs], (it / QST) & 1);  // stats landed with the TMA stage
+      const float4* st4 = reinterpret_cast<const float4*>(smem + kStats + qs * 2 * BQ * 4);
+      mbar_wait(&bars.s_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tmem_ld32(tmem + lane_base + b * 128 + c0, sr);
+      tmem_ld32(tmem + lane_base + b * 128 + 64 + c0, dr);
+      tmem_ld_wait();
+      uint32_t pw[16], dw[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        const float4 l4 = st4[(c0 + c) / 4];
+        const float4 d4 = st4[(BQ + c0 + c) / 4];
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pv[4], dsv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bool keep = key_ok;
+          if (!full) keep = keep && kpos <= qpos[c + e];
+          const float pr = keep ? ex2(fmaf(__uint_as_float(sr[c + e]), sl2, -lv[e])) : 0.f;
+          pv[e] = pr;
+          dsv[e] = pr * scale * (__uint_as_float(dr[c + e]) - dv4[e]);
+        }
+        pw[c / 2] = pack_bf16(pv[0], pv[1]);
+        pw[c / 2 + 1] = pack_bf16(pv[2], pv[3]);
+        dw[c / 2] = pack_bf16(dsv[0], dsv[1]);
+        dw[c / 2 + 1] = pack_bf16(dsv[2], dsv[3]);
+      }
       if (it >= 2) mbar_wait(&bars.pds_free[b], ((it - 2) >> 1) & 1);  // P/dS smem b reusable
       uint8_t* prow = smem + kP + b * 16384;
       uint8_t* dsrow = smem + kDS + b * 16384;
-      const int* qp = p.q_pos + qt * BQ;
 #pragma unroll
-      for (int c8 = 0; c8 < BQ / 8; ++c8) {
-        uint32_t pw[4], dw[4];
-#pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-          float pv[2], dv[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = c8 * 8 + j + e;
-            bool keep = key_ok;
-            if (!full) keep = keep && (qt * BQ + c < p.Tq) && kpos <= __ldg(qp + c);
-            const float pr = keep ? ex2(fmaf(s[c], sl2, -st[c])) : 0.f;
-            pv[e] = pr;
-            dv[e] = pr * (dp[c] - st[BQ + c]) * scale;
-          }
-          pw[j / 2] = pack_bf16(pv[0], pv[1]);
-          dw[j / 2] = pack_bf16(dv[0], dv[1]);
-        }
-        *reinterpret_cast<uint4*>(prow + sw128_offset(r, c8)) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-        *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, c8)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+      for (int c8 = 0; c8 < 4; ++c8) {
+        *reinterpret_cast<uint4*>(prow + sw128_offset(r, hq * 4 + c8)) =
+            make_uint4(pw[4 * c8], pw[4 * c8 + 1], pw[4 * c8 + 2], pw[4 * c8 + 3]);
+        *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, hq * 4 + c8)) =
+            make_uint4(dw[4 * c8], dw[4 * c8 + 1], dw[4 * c8 + 2], dw[4 * c8 + 3]);
       }
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&bars.ds_full[b]);
-      ++it;
-    }
-    // ---------------------------------------------------------- dV epilogue
-    float acc[D];
-    if (it > 0) {
-      mbar_wait(&bars.dkv_full, 0);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld32(tmem + lane_base + 256 + c * 32, rr);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __uint_as_float(rr[j]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < D; ++j) acc[j] = 0.f;
-    }
-    if (key_ok) {
-      float* dst = p.dv + ((size_t)hk * p.Tk + key) * D;
-#pragma unroll
-      for (int c = 0; c < D; c += 4) {
-        float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-        if (p.accumulate_kv) {
-          const float4 o = *reinterpret_cast<const float4*>(dst + c);
-          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-        }
-        *reinterpret_cast<float4*>(dst + c) = v;
-      }
-    }
-  } else if (warp >= 8) {
-    // -------------------------------------------------------------- WG-B: dQ drain
-    const int wq = warp % 4;
-    const int d = wq * 32 + lane;  // TMEM lane of dQ^T == feature index
-    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    int it = 0;
-    for (int i = 0; i < n_iter_max; ++i) {
-      const int g = i / nqt, qt = i % nqt;
-      if (!live(qt)) continue;
-      const int h = hk * p.G + g;
-      const int b = it & 1;
+      // drain this iteration's dQ^T (issued by the MMA warp right after ds_full)
       mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
       tc_fence_after();
-      uint32_t v0[32], v1[32];
-      tmem_ld32(tmem + lane_base + b * 128, v0);
-      tmem_ld32(tmem + lane_base + b * 128 + 32, v1);
+      uint32_t v[32];
+      tmem_ld32(tmem + lane_base + b * 128 + c0, v);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars.dq_empty[b]);
-      float* dst = p.dq_acc + ((size_t)h * p.Tq + qt * BQ) * D + d;
-      const int rows = min(BQ, p.Tq - qt * BQ);
-      if (rows == BQ) {
+      const int q0 = qt * BQ + c0;
+      float* dst = p.dq_acc + ((size_t)h * p.Tq + q0) * D + r;
+      if (q0 + 32 <= p.Tq) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) atomicAdd(dst + (size_t)c * D, __uint_as_float(v0[c]));
-#pragma unroll
-        for (int c = 0; c < 32; ++c) atomicAdd(dst + (size_t)(c + 32) * D, __uint_as_float(v1[c]));
+        for (int c = 0; c < 32; ++c) atomicAdd(dst + (size_t)c * D, __uint_as_float(v[c]));
       } else {
         for (int c = 0; c < 32; ++c)
-          if (c < rows) atomicAdd(dst + (size_t)c * D, __uint_as_float(v0[c]));
-        for (int c = 0; c < 32; ++c)
-          if (c + 32 < rows) atomicAdd(dst + (size_t)(c + 32) * D, __uint_as_float(v1[c]));
+          if (q0 + c < p.Tq) atomicAdd(dst + (size_t)c * D, __uint_as_float(v[c]));
       }
       ++it;
     }
-    // ---------------------------------------------------------- dK epilogue
-    const int r = d;
-    const int key = key0 + r;
-    float acc[D];
+    // ------------------------------------------------ dV (hq=0) / dK (hq=1) epilogue
     if (it > 0) {
       mbar_wait(&bars.dkv_full, 0);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld32(tmem + lane_base + 384 + c * 32, rr);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __uint_as_float(rr[j]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < D; ++j) acc[j] = 0.f;
     }
-    if (key < p.Tk) {
-      float* dst = p.dk + ((size_t)hk * p.Tk + key) * D;
+    float* dst = (hq == 0 ? p.dv : p.dk) + ((size_t)hk * p.Tk + key) * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t rr[32];
+      if (it > 0) {
+        tmem_ld32(tmem + lane_base + 256 + hq * 128 + c * 32, rr);
+        tmem_ld_wait();
+      } else {
 #pragma unroll
-      for (int c = 0; c < D; c += 4) {
-        float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-        if (p.accumulate_kv) {
-          const float4 o = *reinterpret_cast<const float4*>(dst + c);
-          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        for (int j = 0; j < 32; ++j) rr[j] = 0u;
+      }
+      if (key_ok) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 v = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]), __uint_as_float(rr[j + 2]),
+                                 __uint_as_float(rr[j + 3]));
+          float4* d4 = reinterpret_cast<float4*>(dst + c * 32 + j);
+          if (p.accumulate_kv) {
+            const float4 o = *d4;
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          }
+          *d4 = v;
         }
-        *reinterpret_cast<float4*>(dst + c) = v;
       }
     }
   }

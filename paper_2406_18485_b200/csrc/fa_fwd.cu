@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   using namespace fwd;
   using L = FwdSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   __shared__ FwdBars bars;
 
   const int warp = warp_id(), lane = lane_id();
@@ -290,70 +290,66 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
     }
 
     // ---------------------------------------------------------- epilogue
-    float o[D];
     if (it > 0) {
       mbar_wait(&bars.o_full[t], 0);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
+    }
+    const bool alive = l_sum > 0.f;
+    const float inv = alive ? 1.f / l_sum : 0.f;
+    const float lse_blk = alive ? (m_used + __log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+    const size_t lrow = (size_t)h * p.Tq + (row_ok ? row : 0);
+    float wa = 0.f, wb = inv, lse_new = lse_blk;
+    if (p.merge && row_ok) {
+      const float la = p.lse[lrow];
+      const float mx2 = fmaxf(la, lse_blk);
+      if (mx2 == -INFINITY) {
+        lse_new = -INFINITY;
+        wa = 0.f;
+        wb = 0.f;
+      } else {
+        const float ea = la == -INFINITY ? 0.f : __expf(la - mx2);
+        const float eb = lse_blk == -INFINITY ? 0.f : __expf(lse_blk - mx2);
+        const float z = ea + eb;
+        lse_new = mx2 + __logf(z);
+        wa = ea / z;
+        wb = eb / z * inv;
+      }
+    }
+    if (row_ok) p.lse[lrow] = lse_new;
+    float* acc = (p.acc_o && row_ok) ? p.acc_o + ((size_t)h * p.Tq + row) * D : nullptr;
+    __nv_bfloat16* out =
+        (p.out && row_ok) ? p.out + (size_t)h * p.out_stride_h + (size_t)row * p.out_stride_t : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      if (it > 0) {
         tmem_ld32(tO + c * 32, r);
         tmem_ld_wait();
+      } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[c * 32 + i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) r[i] = 0u;
       }
-    } else {
+      if (!row_ok) continue;
 #pragma unroll
-      for (int i = 0; i < D; ++i) o[i] = 0.f;
-    }
-    if (row_ok) {
-      const bool alive = l_sum > 0.f;
-      const float inv = alive ? 1.f / l_sum : 0.f;
-      const float lse_blk = alive ? (m_used + __log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
-      const size_t lrow = (size_t)h * p.Tq + row;
-      float wa = 0.f, wb = inv, lse_new = lse_blk;
-      if (p.merge) {
-        const float la = p.lse[lrow];
-        const float mx2 = fmaxf(la, lse_blk);
-        if (mx2 == -INFINITY) {
-          lse_new = -INFINITY;
-          wa = 0.f;
-          wb = 0.f;
-        } else {
-          const float ea = la == -INFINITY ? 0.f : __expf(la - mx2);
-          const float eb = lse_blk == -INFINITY ? 0.f : __expf(lse_blk - mx2);
-          const float z = ea + eb;
-          lse_new = mx2 + __logf(z);
-          wa = ea / z;
-          wb = eb / z * inv;
-        }
-      }
-      p.lse[lrow] = lse_new;
-      float* acc = p.acc_o ? p.acc_o + ((size_t)h * p.Tq + row) * D : nullptr;
-      __nv_bfloat16* out = p.out ? p.out + (size_t)h * p.out_stride_h + (size_t)row * p.out_stride_t : nullptr;
-#pragma unroll
-      for (int c = 0; c < D; c += 8) {
+      for (int i = 0; i < 32; i += 8) {
         float v[8];
-        if (p.merge) {
-          const float4 a0 = *reinterpret_cast<const float4*>(acc + c);
-          const float4 a1 = *reinterpret_cast<const float4*>(acc + c + 4);
-          v[0] = a0.x * wa + o[c] * wb; v[1] = a0.y * wa + o[c + 1] * wb;
-          v[2] = a0.z * wa + o[c + 2] * wb; v[3] = a0.w * wa + o[c + 3] * wb;
-          v[4] = a1.x * wa + o[c + 4] * wb; v[5] = a1.y * wa + o[c + 5] * wb;
-          v[6] = a1.z * wa + o[c + 6] * wb; v[7] = a1.w * wa + o[c + 7] * wb;
-        } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = o[c + i] * wb;
+        for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[i + e]) * wb;
+        if (p.merge) {
+          const float4 a0 = *reinterpret_cast<const float4*>(acc + c * 32 + i);
+          const float4 a1 = *reinterpret_cast<const float4*>(acc + c * 32 + i + 4);
+          v[0] += a0.x * wa; v[1] += a0.y * wa; v[2] += a0.z * wa; v[3] += a0.w * wa;
+          v[4] += a1.x * wa; v[5] += a1.y * wa; v[6] += a1.z * wa; v[7] += a1.w * wa;
         }
         if (acc) {
-          *reinterpret_cast<float4*>(acc + c) = make_float4(v[0], v[1], v[2], v[3]);
-          *reinterpret_cast<float4*>(acc + c + 4) = make_float4(v[4], v[5], v[6], v[7]);
+          *reinterpret_cast<float4*>(acc + c * 32 + i) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(acc + c * 32 + i + 4) = make_float4(v[4], v[5], v[6], v[7]);
         }
         if (out) {
           uint4 u;
           u.x = pack_bf16(v[0], v[1]); u.y = pack_bf16(v[2], v[3]);
           u.z = pack_bf16(v[4], v[5]); u.w = pack_bf16(v[6], v[7]);
-          *reinterpret_cast<uint4*>(out + c) = u;
+          *reinterpret_cast<uint4*>(out + c * 32 + i) = u;
         }
       }
     }

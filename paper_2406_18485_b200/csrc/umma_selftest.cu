@@ -13,7 +13,7 @@ namespace a2d {
 
 __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const __grid_constant__ SelftestParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint8_t* sA = smem;              // 2 panels x 16 KB
   uint8_t* sB = smem + 32768;      // 2 panels x 16 KB
   uint8_t* sV = smem + 65536;      // MN-major: 2 panels (n 0-63, 64-127) x 16 KB

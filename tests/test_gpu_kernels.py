@@ -184,7 +184,7 @@ def test_permute_and_gather_bit_exact():
     from paper_2406_18485_b200 import kernels as K
     d = dev()
     x = torch.randint(-2**15, 2**15, (4, 3, 40, 16), dtype=torch.int16, device=d).view(torch.bfloat16)
-    y = K.permute_blocks(x, 4, 3)
+    y = K.permute_blocks(x, 4, 3).view(3, 4, 40, 16)
     assert torch.equal(y.view(torch.int16), x.view(torch.int16).permute(1, 0, 2, 3).contiguous())
     idx = torch.tensor([2, 0, 0, 1, 3, 3], dtype=torch.int32, device=d)
     out = torch.empty((6, 3, 40, 16), dtype=torch.bfloat16, device=d)
