@@ -1,0 +1,341 @@
+"""2D-Attention fwd+bwd throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+
+One step = one 2D-Attention layer forward + backward on the global sequence
+(S=131072, H=32, d=128, MHA, causal — BASELINE config 3's shape) through the
+SPMD runtime (``paper_2406_18485_b200.dist.Attn2D``): HP all-to-all, Double-
+Ring attention, all-to-all back, then the backward ring. Inputs are random
+bf16 (synthetic; the path has no weights). Algorithmic FLOPs per step:
+7 * S^2 * H * d (causal fwd 2 S^2 H d + bwd 2.5x), counted on query heads.
+
+`value` is whole-job TFLOP/s with inputs resident in HBM; `e2e` repeats the
+step through the same public API with the step's inputs copied from pinned
+host memory and its gradients (dq, dk, dv) copied back inside the timed
+region. Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2D-Attention fwd+bwd TFLOP/s/GPU (MFU) at S=128K, 1/2/4/8 B200"
+UNIT = "TFLOP/s"
+
+
+def default_grid(n: int):
+    """(d_hp, d_cp, w) per GPU count: BASELINE config 3 is 4x2 at 8 GPUs."""
+    return {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 2), 8: (4, 2, 2)}.get(n, (n, 1, 1))
+
+
+def peaks():
+    p = {"hbm_gbs": 6527.5, "bf16_tflops": 1665.8, "bf16_tflops_sustained": 1389.6, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["src"] = "measured"
+    except OSError:
+        pass
+    return p
+
+
+# --------------------------------------------------------------------- clocks
+REASONS = ["clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+           "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = "index,clocks.sm,clocks.max.sm,power.draw," + ",".join(REASONS)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], None, set()
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 4 + len(REASONS):
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                for name, val in zip(REASONS, parts[4:]):
+                    if val.lower() == "active":
+                        reasons.add(name.split(".")[-1])
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU leg
+def cpu_sample(rows: int, S: int, d: int, seed: int = 0):
+    """Oracle port (oracle/attn2d_oracle.py, f64 numpy/BLAS) on a bounded sample
+    of the workload: 1 head x the last `rows` query positions x all S keys,
+    fwd + bwd. Returns (seconds, algorithmic FLOPs of the sample)."""
+    import numpy as np
+
+    from oracle import attn2d_oracle as orc
+
+    rng = np.random.Generator(np.random.Philox(seed))
+    q = rng.standard_normal((1, rows, d))
+    k = rng.standard_normal((1, S, d))
+    v = rng.standard_normal((1, S, d))
+    do = rng.standard_normal((1, rows, d))
+    qpos = np.arange(S - rows, S)
+    kpos = np.arange(S)
+    t0 = time.perf_counter()
+    orc.attention(q, k, v, qpos, kpos, True)
+    orc.attention_grads(q, k, v, do, qpos, kpos, True)
+    dt = time.perf_counter() - t0
+    admitted = float(sum(int(p) + 1 for p in qpos))  # causal (query, key) pairs
+    flops = 3.5 * 4.0 * admitted * d
+    return dt, flops
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max((i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"), default=1)
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(a, rank: int, world: int):
+    """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
+    if rank != 0:
+        return 0
+    S, H, d = a.seq, a.heads, a.dim
+    rows = a.cpu_rows
+    for _ in range(a.warmup if a.warmup < 1 else 1):
+        cpu_sample(64, S, d)
+    times, flops = [], 0.0
+    for _ in range(a.steps):
+        dt, fl = cpu_sample(rows, S, d)
+        times.append(dt)
+        flops = fl
+    tot = sum(times)
+    val = flops * len(times) / tot / 1e12
+    sample = f"1 head x last {rows} query rows x {S} keys, d={d}, causal fwd+bwd, f64 numpy (oracle port)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": tot / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"2D-Attention fwd+bwd MHA H={H} D={d} S={S} causal (CPU sample)"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seq", type=int, default=131072)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=32)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--d-hp", type=int, default=0)
+    ap.add_argument("--d-cp", type=int, default=0)
+    ap.add_argument("--w", type=int, default=0)
+    ap.add_argument("--placement", default="head_first")
+    ap.add_argument("--cpu-rows", type=int, default=1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world} (launch N>1 with torchrun)")
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_18485_b200 import _lib
+    from paper_2406_18485_b200.config import ClusterConfig, ModelConfig, ParallelConfig, Placement
+    from paper_2406_18485_b200.dist import Attn2D
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29551")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    d_hp, d_cp, w = default_grid(world)
+    d_hp, d_cp = a.d_hp or d_hp, a.d_cp or d_cp
+    w = a.w or (w if (a.d_hp == 0 and a.d_cp == 0) else d_cp)
+    S, H, Hkv, d = a.seq, a.heads, a.kv_heads, a.dim
+    model = ModelConfig(seq_len=S, heads=H, kv_heads=Hkv, hidden=H * d)
+    par = ParallelConfig(d_hp=d_hp, d_cp=d_cp, inner_ring=w, placement=Placement(a.placement))
+    op = Attn2D(model, par, ClusterConfig(), causal=True)
+    L = op.L
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q = torch.randn((H, L, d), device=dev, dtype=torch.bfloat16, generator=g)
+    k = torch.randn((Hkv, L, d), device=dev, dtype=torch.bfloat16, generator=g)
+    v = torch.randn((Hkv, L, d), device=dev, dtype=torch.bfloat16, generator=g)
+    do = torch.randn((H, L, d), device=dev, dtype=torch.bfloat16, generator=g)
+
+    def step():
+        op.forward(q, k, v)
+        return op.backward(do)
+
+    for _ in range(max(a.warmup, 3 if a.warmup >= 3 else a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+
+    # ---------------- timed region: inputs resident in HBM
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.LOG.reset(timed=("a2d_fa_bwd_chunk", "a2d_fa_fwd_chunk"))
+    _lib.LOG.enabled = True
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    _lib.LOG.enabled = False
+    dist.barrier()
+    clk = clocks.stop()
+    t_ms = e0.elapsed_time(e1)
+    launches = _lib.LOG.count // a.steps
+    kern = {"a2d_fa_bwd_chunk": [0.0, 0], "a2d_fa_fwd_chunk": [0.0, 0]}
+    for name, s0, s1 in _lib.LOG.events:
+        kern[name][0] += s0.elapsed_time(s1)
+        kern[name][1] += 1
+    tt = torch.tensor([t_ms, kern["a2d_fa_bwd_chunk"][0], kern["a2d_fa_fwd_chunk"][0]], device=dev,
+                      dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms, bwd_ms, fwd_ms = (float(x) for x in tt.tolist())
+
+    flops = op.flops()
+    value = flops * a.steps / (t_ms * 1e-3) / 1e12
+    ms_step = t_ms / a.steps
+
+    # ---------------- e2e through the same public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        host_in = [x.cpu().pin_memory() for x in (q, k, v, do)]
+        host_out = [torch.empty((H, L, d), dtype=torch.bfloat16).pin_memory(),
+                    torch.empty((Hkv, L, d), dtype=torch.bfloat16).pin_memory(),
+                    torch.empty((Hkv, L, d), dtype=torch.bfloat16).pin_memory()]
+        dev_in = [torch.empty_like(x, device=dev) for x in host_in]
+        h2d = sum(x.numel() * x.element_size() for x in host_in)
+        d2h = sum(x.numel() * x.element_size() for x in host_out)
+
+        def e2e_step():
+            for dst, src in zip(dev_in, host_in):
+                dst.copy_(src, non_blocking=True)
+            op.forward(dev_in[0], dev_in[1], dev_in[2])
+            grads = op.backward(dev_in[3])
+            for dst, src in zip(host_out, grads):
+                dst.copy_(src, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(a.steps):
+            e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops * a.steps / (float(te.item()) * 1e-3) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "ms_per_step": float(te.item()) / a.steps}
+
+    if rank == 0:
+        pk = peaks()
+        per_gpu = value / world
+        # dominant kernel: the backward chunk kernel (algorithmic FLOPs of the
+        # backward = 2.5/3.5 of the step, split evenly over ranks)
+        bwd_launch_flops = flops * (2.5 / 3.5) / world
+        fwd_launch_flops = flops * (1.0 / 3.5) / world
+        bwd_achieved = bwd_launch_flops * a.steps / (bwd_ms * 1e-3) / 1e12 if bwd_ms > 0 else None
+        fwd_achieved = fwd_launch_flops * a.steps / (fwd_ms * 1e-3) / 1e12 if fwd_ms > 0 else None
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tr = json.load(f).get(f"bwd_S{S}_H{H}_d{d}_{d_hp}x{d_cp}")
+                traffic = tr
+        except (OSError, ValueError):
+            pass
+        roof = {"kernel": "a2d_fa_bwd_chunk (fa_bwd_kernel)", "bound": "tensor",
+                "achieved": bwd_achieved, "peak": pk["bf16_tflops_sustained"], "unit": UNIT,
+                "frac": (bwd_achieved / pk["bf16_tflops_sustained"]) if bwd_achieved else None,
+                "frac_of_burst": (bwd_achieved / pk["bf16_tflops"]) if bwd_achieved else None,
+                "peak_kind": f"{pk['src']} sustained (kernel runs inside a long step); burst {pk['bf16_tflops']}",
+                "traffic": traffic,
+                "share_of_step": bwd_ms / t_ms if t_ms else None,
+                "fwd_kernel": {"achieved": fwd_achieved, "share_of_step": fwd_ms / t_ms if t_ms else None}}
+        cpu = None
+        if world == 1 and not a.no_cpu:
+            dt, fl = cpu_sample(a.cpu_rows, S, d)
+            cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+                   "sample": f"1 head x last {a.cpu_rows} query rows x {S} keys, d={d}, causal fwd+bwd, "
+                             f"f64 numpy oracle port, {dt:.2f} s"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random bf16 q/k/v/dO)",
+            "config": {"workload": f"2D-Attention fwd+bwd MHA H={H} H_kv={Hkv} D={d} S={S} causal",
+                       "d_hp": d_hp, "d_cp": d_cp, "w": w, "placement": a.placement,
+                       "global_tokens": S, "l2": "inputs > L2 (each q/k/v tensor >= 128 MiB per rank), no flush"},
+            "tflops_per_gpu": per_gpu, "mfu": per_gpu / pk["bf16_tflops"],
+            "mfu_sustained": per_gpu / pk["bf16_tflops_sustained"],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -84,9 +84,12 @@ int a2d_merge(float* acc_o, float* acc_lse, const float* blk_o, const float* blk
  * unpack/pack (ref seq_alltoall_scatter / gather, sharding.py:131-169). */
 int a2d_permute_blocks(const void* src, void* dst, int64_t A, int64_t B, int64_t block_bytes, void* stream);
 
-/* dst[i][:] = src[map[i]][:] — GQA KV replication by addressing
- * (ref kv_replicate, sharding.py:109-128). map is a device int32 array. */
-int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, int64_t n, int64_t block_bytes, void* stream);
+/* dst[dst_map ? dst_map[i] : i][:] = src[map[i]][:] for n blocks — the
+ * SeqAlltoAll send-buffer pack with GQA KV replication done by addressing
+ * (ref kv_replicate, sharding.py:109-128). Maps are device int32 arrays;
+ * dst_map may be NULL. */
+int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, const int32_t* dst_map, int64_t n,
+                      int64_t block_bytes, void* stream);
 
 /* dst[h] = sum_r src[h*rep + r] over per_head fp32 values (gradient of kv_replicate). */
 int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream);

@@ -25,7 +25,7 @@ SIGNATURES = {
                          _c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_f32, _vp],
     "a2d_merge": [_vp, _vp, _vp, _vp, _c_i64, _c_i32, _vp],
     "a2d_permute_blocks": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp],
-    "a2d_gather_blocks": [_vp, _vp, _vp, _c_i64, _c_i64, _vp],
+    "a2d_gather_blocks": [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp],
     "a2d_sum_replicas_f32": [_vp, _vp, _c_i64, _c_i32, _c_i64, _vp],
     "a2d_f32_to_bf16": [_vp, _vp, _c_i64, _vp],
     "a2d_add_f32": [_vp, _vp, _c_i64, _vp],
@@ -59,10 +59,45 @@ def load(path: str = LIB_PATH):
     return lib
 
 
+# kernels each entry point launches (for the bench's gpu_launches accounting)
+LAUNCHES = {"a2d_tile_bounds": 1, "a2d_fa_fwd_chunk": 1, "a2d_bwd_preprocess": 1, "a2d_fa_bwd_chunk": 1,
+            "a2d_merge": 1, "a2d_permute_blocks": 1, "a2d_gather_blocks": 1, "a2d_sum_replicas_f32": 1,
+            "a2d_f32_to_bf16": 1, "a2d_add_f32": 1, "a2d_selftest_umma": 1}
+
+
+class LaunchLog:
+    """Counts library kernel launches; optionally brackets chosen entry points
+    with CUDA events recorded on the launching (current) stream."""
+
+    def __init__(self):
+        self.enabled = False
+        self.count = 0
+        self.timed: set[str] = set()
+        self.events: list = []  # (name, start_event, end_event)
+
+    def reset(self, timed=()):
+        self.count = 0
+        self.timed = set(timed)
+        self.events = []
+
+
+LOG = LaunchLog()
+
+
 def call(name: str, *args) -> None:
     """Invoke an entry point; map non-zero status to ValueError / KernelError."""
     lib = load()
+    ev = None
+    if LOG.enabled:
+        LOG.count += LAUNCHES.get(name, 0)
+        if name in LOG.timed:
+            import torch
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
     rc = getattr(lib, name)(*args)
+    if ev is not None:
+        ev[1].record()
+        LOG.events.append((name, ev[0], ev[1]))
     if rc != 0:
         msg = lib.a2d_last_error().decode()
         if rc == 1:

@@ -153,23 +153,26 @@ cudaError_t launch_permute_blocks(const void* src, void* dst, int64_t A, int64_t
 }
 
 __global__ void gather_blocks_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
-                                     const int* __restrict__ map, int64_t n, int64_t blk_vec) {
+                                     const int* __restrict__ map, const int* __restrict__ dmap, int64_t n,
+                                     int64_t blk_vec) {
   const int64_t total = n * blk_vec;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t blk = i / blk_vec, e = i % blk_vec;
-    dst[i] = __ldg(src + (int64_t)map[blk] * blk_vec + e);
+    const int64_t d = dmap ? (int64_t)dmap[blk] : blk;
+    dst[d * blk_vec + e] = __ldg(src + (int64_t)map[blk] * blk_vec + e);
   }
 }
 
-cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, int64_t n, int64_t blk_bytes, int n_sm,
-                                 cudaStream_t s) {
+// dst[dmap ? dmap[i] : i] = src[map[i]] for n blocks.
+cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, const int* dmap, int64_t n,
+                                 int64_t blk_bytes, int n_sm, cudaStream_t s) {
   if (blk_bytes % 16 != 0) return cudaErrorInvalidValue;
   const int64_t total = n * (blk_bytes / 16);
   if (total == 0) return cudaSuccess;
   int64_t blocks = (total + 255) / 256;
   if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
   gather_blocks_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), map,
-                                                        n, blk_bytes / 16);
+                                                        dmap, n, blk_bytes / 16);
   return cudaGetLastError();
 }
 

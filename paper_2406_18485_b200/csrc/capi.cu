@@ -21,8 +21,8 @@ cudaError_t launch_merge_f32(float* acc_o, float* acc_lse, const float* blk_o, c
                              int D, cudaStream_t s);
 cudaError_t launch_permute_blocks(const void* src, void* dst, int64_t A, int64_t B, int64_t blk_bytes, int n_sm,
                                   cudaStream_t s);
-cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, int64_t n, int64_t blk_bytes, int n_sm,
-                                 cudaStream_t s);
+cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, const int* dmap, int64_t n,
+                                 int64_t blk_bytes, int n_sm, cudaStream_t s);
 cudaError_t launch_sum_replicas(const float* src, float* dst, int64_t heads, int rep, int64_t per_head, int n_sm,
                                 cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, int n_sm, cudaStream_t s);
@@ -202,9 +202,11 @@ int a2d_permute_blocks(const void* src, void* dst, int64_t A, int64_t B, int64_t
   return cuda_status(launch_permute_blocks(src, dst, A, B, block_bytes, sm_count(), S(stream)), "a2d_permute_blocks");
 }
 
-int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, int64_t n, int64_t block_bytes, void* stream) {
+int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, const int32_t* dst_map, int64_t n,
+                      int64_t block_bytes, void* stream) {
   if (n < 0 || block_bytes % 16 != 0) return fail(A2D_EINVAL, "a2d_gather_blocks: block_bytes % 16 != 0");
-  return cuda_status(launch_gather_blocks(src, dst, map, n, block_bytes, sm_count(), S(stream)), "a2d_gather_blocks");
+  return cuda_status(launch_gather_blocks(src, dst, map, dst_map, n, block_bytes, sm_count(), S(stream)),
+                     "a2d_gather_blocks");
 }
 
 int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream) {

@@ -1,0 +1,406 @@
+"""SPMD 2D-Attention runtime: one process per GPU, NCCL over NVLink.
+
+Alg. 1 of the paper (ref ``ring.py:82-119``) executed for real:
+
+  SeqSharded q/k/v (H, L, d) per rank
+    -> pack (128-bit gather kernel; GQA replication by addressing)
+    -> NCCL all-to-all inside the HP group (d_hp ranks sharing a cp_index)
+    -> unpack (128-bit permute kernel) = HeadSharded (H/d_hp, C, d)
+    -> Double-Ring attention inside the CP group (d_cp ranks sharing an
+       hp_index): KV chunks rotate over an inner ring of size w and an outer
+       ring of d_cp/w, as NCCL send/recv on two separate communicators so an
+       outer hop (issued at the start of an outer step) overlaps the w inner
+       hops and the attention kernels (Alg. 2);
+       each step folds its block into an fp32 accumulator inside the
+       attention kernel's epilogue
+    -> pack + NCCL all-to-all back -> SeqSharded output (H, L, d)
+
+Backward (not in the reference; designed here and checked
+against the global oracle): KV chunks rotate again along the same schedule;
+a travelling fp32 dK/dV accumulator follows each chunk one step behind and
+is added to (K4 kernel) by every rank that consumes the chunk. The
+accumulator's hop is (r, p) -> (r, p+1) inside an outer step and the
+"diagonal" (r, p) -> (r+1, p+1) across outer steps; the same diagonal hop
+after the last step brings every accumulator home to its owner.
+
+All comm runs on NCCL's internal streams; ``Work.wait()`` only makes the
+compute stream wait (no host sync).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import kernels as K
+from .config import (ClusterConfig, ModelConfig, ParallelConfig, build_rank_grid,
+                     check_config, replicated_kv_heads)
+from .layout import cp_positions, replica_source_heads, seq_positions
+from .schedule import build_ring_schedule
+
+
+@dataclass
+class StepTimes:
+    """CUDA events per phase of the last call (for bench / exposed-comm)."""
+
+    events: list = field(default_factory=list)
+
+    def mark(self, name: str):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.events.append((name, e))
+
+    def clear(self):
+        self.events.clear()
+
+
+class Attn2D:
+    """Per-rank 2D-Attention operator (HP all-to-all x Double-Ring CP).
+
+    ``forward(q, k, v)`` takes this rank's SeqSharded chunks
+    (H, L, d) / (H_kv, L, d) in the zig-zag token order of
+    ``layout.seq_positions`` and returns the SeqSharded output (H, L, d).
+    ``backward(dout)`` returns (dq, dk, dv) in the same layout.
+    """
+
+    def __init__(self, model: ModelConfig, par: ParallelConfig, cluster: ClusterConfig | None = None,
+                 causal: bool = True, group=None, device=None):
+        cluster = cluster or ClusterConfig()
+        check_config(model, par, cluster)
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed must be initialised (one rank per GPU)")
+        self.model, self.par, self.causal = model, par, causal
+        self.grid = build_rank_grid(par, cluster)
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world != self.grid.d_sp:
+            raise ValueError(f"world size {self.world} != d_hp*d_cp = {self.grid.d_sp}")
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.hp, self.cp = self.grid.coords_of(self.rank)
+        d_hp, d_cp, w = par.d_hp, par.d_cp, par.inner_ring
+        S, H, Hkv = model.seq_len, model.heads, model.kv_heads
+        self.d = model.head_dim
+        self.kd = K.fwd_dim(self.d)
+        self.bd = K.BWD_DIM
+        self.scale = 1.0 / math.sqrt(self.d)
+        self.H_rep = replicated_kv_heads(Hkv, d_hp, H)
+        if self.H_rep % d_hp != 0:
+            raise ValueError(f"{self.H_rep} heads not divisible by d_hp={d_hp}")
+        self.Hl, self.Hkl = H // d_hp, self.H_rep // d_hp
+        self.rep = self.H_rep // Hkv
+        self.L, self.C = S // self.grid.d_sp, S // d_cp
+
+        # ---- process groups (created by every rank, in the same order)
+        self.hp_group = None
+        self.ring_inner = self.ring_outer = self.ring_dkv = None
+        base = group  # None = WORLD
+        g_ranks = list(range(self.world)) if base is None else dist.get_process_group_ranks(base)
+        for j in range(d_cp):
+            ranks = [g_ranks[r] for r in self.grid.hp_group(j)]
+            g = dist.new_group(ranks) if d_hp > 1 else None
+            if j == self.cp:
+                self.hp_group = g
+        for i in range(d_hp):
+            ranks = [g_ranks[r] for r in self.grid.cp_group(i)]
+            gi = dist.new_group(ranks) if d_cp > 1 else None
+            go = dist.new_group(ranks) if d_cp > 1 else None
+            gd = dist.new_group(ranks) if d_cp > 1 else None
+            if i == self.hp:
+                self.ring_inner, self.ring_outer, self.ring_dkv = gi, go, gd
+        self._g = g_ranks
+
+        # ---- schedule and peers (global ranks)
+        self.schedule = build_ring_schedule(d_cp, w)
+        self.steps = self.schedule.steps[self.cp]
+        n = d_cp // w
+        ring, pos = divmod(self.cp, w)
+
+        def cp_rank(r, p):
+            return self._g[self.grid.rank_of(self.hp, (r % n) * w + (p % w))]
+
+        self.inner_to, self.inner_from = cp_rank(ring, pos + 1), cp_rank(ring, pos - 1)
+        self.outer_to, self.outer_from = cp_rank(ring + 1, pos), cp_rank(ring - 1, pos)
+        self.diag_to, self.diag_from = cp_rank(ring + 1, pos + 1), cp_rank(ring - 1, pos - 1)
+
+        # ---- positions / tile plans (device)
+        dev = self.device
+        self.seq_pos = seq_positions(S, self.grid, self.hp, self.cp)
+        self.plans = [K.ChunkPlan(torch.as_tensor(cp_positions(S, d_cp, j), dtype=torch.int32, device=dev))
+                      for j in range(d_cp)]
+        # pack maps for the KV all-to-all: destination block (peer, t, hl) of
+        # [d_hp][2][Hkl] reads original head src(peer*Hkl + hl) of k (t=0) or v (t=1)
+        src = replica_source_heads(Hkv, self.H_rep)
+        dmap_k, dmap_v, smap = [], [], []
+        for peer in range(d_hp):
+            for hl in range(self.Hkl):
+                smap.append(int(src[peer * self.Hkl + hl]))
+                dmap_k.append(peer * 2 * self.Hkl + hl)
+                dmap_v.append(peer * 2 * self.Hkl + self.Hkl + hl)
+        self._smap = torch.tensor(smap, dtype=torch.int32, device=dev)
+        self._dmap_k = torch.tensor(dmap_k, dtype=torch.int32, device=dev)
+        self._dmap_v = torch.tensor(dmap_v, dtype=torch.int32, device=dev)
+        self._bufs: dict = {}
+        self.times = StepTimes()
+        self.record_times = False
+        self.saved = None
+
+    # ------------------------------------------------------------ helpers
+    def _buf(self, name: str, shape, dtype) -> torch.Tensor:
+        key = (name, tuple(shape), dtype)
+        t = self._bufs.get(key)
+        if t is None:
+            t = torch.empty(shape, dtype=dtype, device=self.device)
+            self._bufs[key] = t
+        return t
+
+    def _mark(self, name):
+        if self.record_times:
+            self.times.mark(name)
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor):
+        dist.all_to_all_single(out, inp, group=self.hp_group)
+
+    def _scatter_q(self, x: torch.Tensor, name: str, dk: int) -> torch.Tensor:
+        """SeqSharded (H, L, d) -> HeadSharded (Hl, C, dk) bf16."""
+        x = K.pad_dim(x, dk)
+        d_hp = self.par.d_hp
+        if d_hp == 1:
+            return x
+        recv = self._buf(name + ".recv", (d_hp, self.Hl, self.L, dk), torch.bfloat16)
+        self._a2a(recv, x)
+        out = self._buf(name, (self.Hl, self.C, dk), torch.bfloat16)
+        return K.permute_blocks(recv, d_hp, self.Hl, out=out)
+
+    def _scatter_kv(self, k: torch.Tensor, v: torch.Tensor, name: str, dk: int) -> torch.Tensor:
+        """SeqSharded k, v (H_kv, L, d) -> HeadSharded KV chunk (2, Hkl, C, dk) bf16."""
+        k, v = K.pad_dim(k, dk), K.pad_dim(v, dk)
+        d_hp = self.par.d_hp
+        send = self._buf(name + ".send", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16)
+        K.gather_blocks(k, self._smap, send, self._dmap_k)
+        K.gather_blocks(v, self._smap, send, self._dmap_v)
+        if d_hp == 1:
+            return send.view(2, self.Hkl, self.C, dk)
+        recv = self._buf(name + ".recv", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16)
+        self._a2a(recv, send)
+        out = self._buf(name, (2, self.Hkl, self.C, dk), torch.bfloat16)
+        return K.permute_blocks(recv, d_hp, 2 * self.Hkl, out=out)
+
+    def _gather(self, x: torch.Tensor, name: str) -> torch.Tensor:
+        """HeadSharded (B, C, e) -> SeqSharded (d_hp*B, L, e), any dtype."""
+        d_hp = self.par.d_hp
+        if d_hp == 1:
+            return x
+        B = x.shape[0]
+        send = self._buf(name + ".send", (d_hp, B) + (self.L,) + tuple(x.shape[2:]), x.dtype)
+        K.permute_blocks(x.contiguous(), B, d_hp, out=send)
+        recv = self._buf(name + ".recv", send.shape, x.dtype)
+        self._a2a(recv, send)
+        return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
+
+    def _p2p(self, group, send_t, to, recv_t, frm):
+        ops = [dist.P2POp(dist.isend, send_t, to, group), dist.P2POp(dist.irecv, recv_t, frm, group)]
+        return dist.batch_isend_irecv(ops)
+
+    @staticmethod
+    def _wait(works):
+        for wk in works or ():
+            wk.wait()
+
+    # ------------------------------------------------------------ ring forward
+    def _ring_forward(self, qh, kv_own, out_h, lse):
+        d_cp, w = self.par.d_cp, self.par.inner_ring
+        qplan = self.plans[self.cp]
+        kd = qh.shape[-1]
+        if d_cp == 1:
+            K.fwd_chunk(qh, kv_own[0], kv_own[1], qplan, self.plans[self.cp], self.causal, self.scale,
+                        lse, None, out_h)
+            return
+        acc = self._buf("fwd.acc", (self.Hl, self.C, kd), torch.float32)
+        inner = [self._buf(f"kv.in{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
+        outer = [self._buf(f"kv.out{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
+        cur, first = kv_own, kv_own
+        w_in = w_out = None
+        n_out = 0
+        for s, step in enumerate(self.steps):
+            t = step.inner
+            o = step.outer
+            if t == 0 and o + 1 < d_cp // w:
+                nxt_outer = outer[n_out % 2]
+                n_out += 1
+                w_out = self._p2p(self.ring_outer, first, self.outer_to, nxt_outer, self.outer_from)
+            if t + 1 < w:
+                nxt_inner = inner[(t + 1) % 2]
+                w_in = self._p2p(self.ring_inner, cur, self.inner_to, nxt_inner, self.inner_from)
+            last = s == d_cp - 1
+            K.fwd_chunk(qh, cur[0], cur[1], qplan, self.plans[step.source], self.causal, self.scale, lse, acc,
+                        out_h if last else None, merge=s > 0)
+            self._mark(f"fwd.step{s}")
+            if t + 1 < w:
+                self._wait(w_in)
+                cur = nxt_inner
+            elif not last:
+                self._wait(w_out)
+                cur = first = nxt_outer
+
+    # ------------------------------------------------------------ ring backward
+    def _ring_backward(self, qh, kv_own, doh, lse2, delta, dq_acc):
+        d_cp, w = self.par.d_cp, self.par.inner_ring
+        qplan = self.plans[self.cp]
+        shape = (2, self.Hkl, self.C, self.bd)
+        if d_cp == 1:
+            dkv = self._buf("bwd.dkv_home", shape, torch.float32)
+            K.bwd_chunk(qh, kv_own[0], kv_own[1], doh, qplan, self.plans[self.cp], lse2, delta, dq_acc,
+                        dkv[0], dkv[1], False, self.causal, self.scale)
+            return dkv
+        part = self._buf("bwd.part", shape, torch.float32)
+        acc = [self._buf(f"bwd.acc{i}", shape, torch.float32) for i in range(2)]
+        home = self._buf("bwd.dkv_home", shape, torch.float32)
+        inner = [self._buf(f"kvb.in{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
+        outer = [self._buf(f"kvb.out{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
+        cur, first = kv_own, kv_own
+        w_in = w_out = w_dkv = None
+        n_out = 0
+        for s, step in enumerate(self.steps):
+            t, o = step.inner, step.outer
+            if t == 0 and o + 1 < d_cp // w:
+                nxt_outer = outer[n_out % 2]
+                n_out += 1
+                w_out = self._p2p(self.ring_outer, first, self.outer_to, nxt_outer, self.outer_from)
+            if t + 1 < w:
+                nxt_inner = inner[(t + 1) % 2]
+                w_in = self._p2p(self.ring_inner, cur, self.inner_to, nxt_inner, self.inner_from)
+            # partial dK/dV of the visiting chunk (no dependency on the travelling accumulator)
+            tgt = acc[s % 2] if s == 0 else part
+            K.bwd_chunk(qh, cur[0], cur[1], doh, qplan, self.plans[step.source], lse2, delta, dq_acc,
+                        tgt[0], tgt[1], False, self.causal, self.scale)
+            if s > 0:
+                self._wait(w_dkv)            # accumulator of this chunk arrived in acc[s % 2]
+                K.add_(acc[s % 2], part)     # K4: accumulate ...
+            self._mark(f"bwd.step{s}")
+            # ... and forward: next consumer is (r, p+1) inside an outer step, (r+1, p+1) across
+            last = s == d_cp - 1
+            if last:
+                to, frm, dst = self.diag_to, self.diag_from, home
+            elif (s + 1) % w != 0:
+                to, frm, dst = self.inner_to, self.inner_from, acc[(s + 1) % 2]
+            else:
+                to, frm, dst = self.diag_to, self.diag_from, acc[(s + 1) % 2]
+            w_dkv = self._p2p(self.ring_dkv, acc[s % 2], to, dst, frm)
+            if t + 1 < w:
+                self._wait(w_in)
+                cur = nxt_inner
+            elif not last:
+                self._wait(w_out)
+                cur = first = nxt_outer
+        self._wait(w_dkv)
+        return home
+
+    # ------------------------------------------------------------ public
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+        """SeqSharded bf16 q (H, L, d), k/v (H_kv, L, d) -> SeqSharded out (H, L, d)."""
+        H, L, d = q.shape
+        if (H, L, d) != (self.model.heads, self.L, self.d):
+            raise ValueError(f"q must be (H={self.model.heads}, L={self.L}, d={self.d}), got {tuple(q.shape)}")
+        if tuple(k.shape) != (self.model.kv_heads, self.L, self.d) or k.shape != v.shape:
+            raise ValueError("k/v must be (H_kv, L, d)")
+        self.times.clear()
+        self._mark("fwd.start")
+        kd = self.kd
+        qh = self._scatter_q(q, "q", kd)
+        kvh = self._scatter_kv(k, v, "kv", kd)
+        self._mark("fwd.a2a_in")
+        out_h = self._buf("out_h", (self.Hl, self.C, kd), torch.bfloat16)
+        lse = self._buf("lse", (self.Hl, self.C), torch.float32)
+        self._ring_forward(qh, kvh, out_h, lse)
+        out = self._gather(out_h, "out")
+        self._mark("fwd.a2a_out")
+        self.saved = (qh, kvh, out_h, lse)
+        return out[..., :self.d] if kd != self.d else out
+
+    def backward(self, dout: torch.Tensor):
+        """SeqSharded dout (H, L, d) -> (dq, dk, dv) SeqSharded, bf16."""
+        if self.saved is None:
+            raise RuntimeError("backward called before forward")
+        qh, kvh, out_h, lse = self.saved
+        self._mark("bwd.start")
+        bd = self.bd
+        if self.kd != bd:  # head dim <= 64: the backward kernel runs at 128 (exact zero padding)
+            qh, kvh, out_h = K.pad_dim(qh, bd), K.pad_dim(kvh, bd), K.pad_dim(out_h, bd)
+        out_b = out_h
+        doh = self._scatter_q(dout, "do", bd)
+        self._mark("bwd.a2a_in")
+        lse2, delta = K.bwd_preprocess(out_b, doh, lse)
+        dq_acc = self._buf("dq_acc", (self.Hl, self.C, bd), torch.float32)
+        dq_acc.zero_()
+        dkv = self._ring_backward(qh, kvh, doh, lse2, delta, dq_acc)
+        self._mark("bwd.ring")
+        dq = self._gather(K.to_bf16(dq_acc, self._buf("dq_h", dq_acc.shape, torch.bfloat16)), "dq")
+        if self.rep == 1:
+            dkv_b = K.to_bf16(dkv, self._buf("dkv_h", dkv.shape, torch.bfloat16))
+            g = self._gather_kv(dkv_b, "dkv")
+            dk, dv = g[0], g[1]
+        else:
+            g = self._gather_kv(dkv, "dkv32")
+            dk = K.to_bf16(K.sum_replicas(g[0].contiguous(), self.rep))
+            dv = K.to_bf16(K.sum_replicas(g[1].contiguous(), self.rep))
+        self._mark("bwd.a2a_out")
+        sl = (lambda x: x[..., :self.d]) if bd != self.d else (lambda x: x)
+        return sl(dq), sl(dk), sl(dv)
+
+    def _gather_kv(self, x: torch.Tensor, name: str) -> torch.Tensor:
+        """HeadSharded (2, Hkl, C, e) -> SeqSharded (2, H_rep, L, e)."""
+        d_hp = self.par.d_hp
+        if d_hp == 1:
+            return x
+        e = x.shape[-1]
+        flat = x.reshape(2 * self.Hkl, self.C, e)
+        g = self._gather(flat, name)                       # [peer][2][Hkl][L][e]
+        out = self._buf(name + ".kv", (2, d_hp, self.Hkl, self.L, e), x.dtype)
+        K.permute_blocks(g.view(d_hp, 2, self.Hkl, self.L, e), d_hp, 2, out=out)
+        return out.view(2, self.H_rep, self.L, e)
+
+    def flops(self) -> float:
+        """Algorithmic fwd+bwd FLOPs of the whole layer (all ranks): 3.5 x 4 S^2 H d x (1/2 if causal)."""
+        S, H = self.model.seq_len, self.model.heads
+        return 3.5 * 4.0 * S * S * H * self.d * (0.5 if self.causal else 1.0)
+
+
+class Attn2DFunction(torch.autograd.Function):
+    """autograd wrapper: saves O and LSE (selective-checkpoint friendly), no recompute of attention."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, op: Attn2D):
+        ctx.op = op
+        return op.forward(q, k, v)
+
+    @staticmethod
+    def backward(ctx, dout):
+        dq, dk, dv = ctx.op.backward(dout.contiguous())
+        return dq, dk, dv, None
+
+
+def shard_global(x: torch.Tensor, op: Attn2D) -> torch.Tensor:
+    """This rank's SeqSharded chunk of a global (H, S, d) tensor (ref shard_sequence)."""
+    idx = torch.as_tensor(op.seq_pos, device=x.device)
+    return x[:, idx].contiguous()
+
+
+def unshard_global(chunks: list[torch.Tensor], op: Attn2D) -> torch.Tensor:
+    """Reassemble global (H, S, d) from all ranks' SeqSharded chunks (ref unshard)."""
+    S = op.model.seq_len
+    out = torch.empty((chunks[0].shape[0], S) + tuple(chunks[0].shape[2:]), dtype=chunks[0].dtype,
+                      device=chunks[0].device)
+    for r, c in enumerate(chunks):
+        hp, cp = op.grid.coords_of(r)
+        idx = torch.as_tensor(seq_positions(S, op.grid, hp, cp), device=c.device)
+        out[:, idx] = c
+    return out
+
+
+def positions_of_rank(op: Attn2D, rank: int) -> np.ndarray:
+    hp, cp = op.grid.coords_of(rank)
+    return seq_positions(op.model.seq_len, op.grid, hp, cp)

@@ -18,14 +18,6 @@ FWD_DIMS = (64, 128)
 BWD_DIM = 128
 
 
-def _ptr(t):
-    return None if t is None else ctypes_ptr(t)
-
-
-def ctypes_ptr(t: torch.Tensor) -> int:
-    return t.data_ptr()
-
-
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -139,11 +131,16 @@ def permute_blocks(src: torch.Tensor, A: int, B: int, out: torch.Tensor | None =
     return out
 
 
-def gather_blocks(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
-    """out[i] = src[index[i]] over leading-dim blocks."""
-    blk = src[0].numel() * src.element_size()
+def gather_blocks(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor,
+                  dst_index: torch.Tensor | None = None, block_elems: int | None = None) -> torch.Tensor:
+    """out[dst_index[i] or i] = src[index[i]] over blocks (default: leading-dim slices)."""
+    if block_elems is None:
+        block_elems = src[0].numel()
+    blk = block_elems * src.element_size()
     idx = index.to(device=src.device, dtype=torch.int32).contiguous()
-    _lib.call("a2d_gather_blocks", src.data_ptr(), out.data_ptr(), idx.data_ptr(), idx.numel(), blk, _stream())
+    didx = None if dst_index is None else dst_index.to(device=src.device, dtype=torch.int32).contiguous()
+    _lib.call("a2d_gather_blocks", src.data_ptr(), out.data_ptr(), idx.data_ptr(),
+              None if didx is None else didx.data_ptr(), idx.numel(), blk, _stream())
     return out
 
 

@@ -1,0 +1,72 @@
+"""Multi-GPU parity of the distributed runtime vs the CPU oracle.
+
+Each case launches ``tests/dist_check.py`` under torchrun with one rank per
+GPU (skipped when the box has fewer GPUs than the case needs). Tolerance
+(bf16 outputs vs the f64 oracle): max-abs <= 2e-2 * max(1, max|ref|) and
+rel-L2 <= 1e-2 for O, dQ, dK, dV. The range factor matters only for
+gradients whose magnitude exceeds 1 (bf16 keeps 8 mantissa bits).
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MAX_ABS, REL_L2 = 2e-2, 1e-2
+
+CASES = [
+    # d_hp, d_cp, w, placement, H, H_kv, S, d
+    (2, 1, 1, "head_first", 8, 8, 1024, 128),
+    (1, 2, 2, "head_first", 8, 8, 1024, 128),
+    (1, 2, 1, "context_first", 4, 2, 1024, 128),
+    (2, 2, 2, "head_first", 8, 2, 2048, 128),
+    (2, 2, 1, "context_first", 8, 8, 2048, 128),
+    (1, 4, 2, "head_first", 4, 4, 2048, 128),
+    (1, 4, 4, "context_first", 4, 1, 2048, 128),
+    (4, 1, 1, "head_first", 8, 2, 1024, 128),  # GQA replication: H_kv=2 < d_hp=4
+    (2, 2, 2, "context_first", 8, 8, 1024, 64),
+]
+
+
+def _run(nproc, args, tmp_path):
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "dist_check.py"),
+           *args, "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return json.loads(out.read_text())
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[:3])) + f"-{c[3]}-H{c[4]}-{c[5]}-S{c[6]}-d{c[7]}")
+def test_dist_matches_oracle(case, tmp_path):
+    d_hp, d_cp, w, pl, H, Hkv, S, d = case
+    n = d_hp * d_cp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    res = _run(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
+                   "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", str(d)], tmp_path)
+    for name in ("O", "dQ", "dK", "dV"):
+        ma, rl, rng = res[name]
+        assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
+            f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
+
+
+@pytest.mark.parametrize("placement", ["head_first", "context_first"])
+def test_dist_golden_config1_shape(placement, tmp_path):
+    """Reference run_2d_attention output (golden) at a config-1 shape: H=8 d=64 S=512, 2x2, w=2."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    res = _run(4, ["--d-hp", "2", "--d-cp", "2", "--w", "2", "--placement", placement, "--heads", "8",
+                   "--kv-heads", "8", "--seq", "512", "--dim", "64",
+                   "--golden", os.path.join(ROOT, "tests", "golden", "gpu_pipeline_c1s.npz")], tmp_path)
+    for name in ("O", "O_golden"):
+        ma, rl, rng = res[name]
+        assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
+            f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"

@@ -11,6 +11,7 @@ ap.add_argument("--Hkv", type=int, default=32)
 ap.add_argument("--D", type=int, default=128)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--causal", type=int, default=1)
+ap.add_argument("--only", default="")
 a = ap.parse_args()
 dev = torch.device("cuda")
 torch.manual_seed(0)
@@ -43,7 +44,8 @@ def timeit(fn):
 c = 0.5 if a.causal else 1.0
 f_fwd = 4 * S * S * H * D * c
 f_bwd = 2.5 * f_fwd
-tf = timeit(fwd); tb = timeit(bwd)
+tf = timeit(fwd) if a.only != 'bwd' else 1.0
+tb = timeit(bwd) if a.only != 'fwd' else 1.0
 print(json.dumps({"S": S, "H": H, "Hkv": Hkv, "D": D, "causal": a.causal,
     "fwd_ms": round(tf, 3), "fwd_tflops": round(f_fwd / tf / 1e9, 1),
     "bwd_ms": round(tb, 3), "bwd_tflops": round(f_bwd / tb / 1e9, 1),
