@@ -40,7 +40,7 @@ from . import kernels as K
 from .config import (ClusterConfig, ModelConfig, ParallelConfig, build_rank_grid,
                      check_config, replicated_kv_heads)
 from .layout import cp_positions, replica_source_heads, seq_positions
-from .schedule import build_ring_schedule
+from .schedule import build_ring_schedule, dkv_hop, ring_peers
 
 
 @dataclass
@@ -116,15 +116,14 @@ class Attn2D:
         # ---- schedule and peers (global ranks)
         self.schedule = build_ring_schedule(d_cp, w)
         self.steps = self.schedule.steps[self.cp]
-        n = d_cp // w
-        ring, pos = divmod(self.cp, w)
+        pe = ring_peers(self.cp, d_cp, w)
 
-        def cp_rank(r, p):
-            return self._g[self.grid.rank_of(self.hp, (r % n) * w + (p % w))]
+        def cp_rank(j):
+            return self._g[self.grid.rank_of(self.hp, j)]
 
-        self.inner_to, self.inner_from = cp_rank(ring, pos + 1), cp_rank(ring, pos - 1)
-        self.outer_to, self.outer_from = cp_rank(ring + 1, pos), cp_rank(ring - 1, pos)
-        self.diag_to, self.diag_from = cp_rank(ring + 1, pos + 1), cp_rank(ring - 1, pos - 1)
+        self.inner_to, self.inner_from = cp_rank(pe.inner_to), cp_rank(pe.inner_from)
+        self.outer_to, self.outer_from = cp_rank(pe.outer_to), cp_rank(pe.outer_from)
+        self.diag_to, self.diag_from = cp_rank(pe.diag_to), cp_rank(pe.diag_from)
 
         # ---- positions / tile plans (device)
         dev = self.device
@@ -283,12 +282,11 @@ class Attn2D:
             self._mark(f"bwd.step{s}")
             # ... and forward: next consumer is (r, p+1) inside an outer step, (r+1, p+1) across
             last = s == d_cp - 1
-            if last:
-                to, frm, dst = self.diag_to, self.diag_from, home
-            elif (s + 1) % w != 0:
-                to, frm, dst = self.inner_to, self.inner_from, acc[(s + 1) % 2]
+            dst = home if last else acc[(s + 1) % 2]
+            if dkv_hop(s, d_cp, w) == "inner":
+                to, frm = self.inner_to, self.inner_from
             else:
-                to, frm, dst = self.diag_to, self.diag_from, acc[(s + 1) % 2]
+                to, frm = self.diag_to, self.diag_from
             w_dkv = self._p2p(self.ring_dkv, acc[s % 2], to, dst, frm)
             if t + 1 < w:
                 self._wait(w_in)

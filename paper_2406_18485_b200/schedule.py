@@ -121,6 +121,67 @@ def home_transfer(j: int, schedule: RingSchedule) -> Transfer:
     return Transfer("home", last, sender)
 
 
+@dataclass(frozen=True)
+class RingPeers:
+    """CP-rank indices one rank talks to (all hops are fixed permutations)."""
+
+    inner_to: int
+    inner_from: int
+    outer_to: int
+    outer_from: int
+    diag_to: int     # dK/dV accumulator hop across outer steps and the home hop
+    diag_from: int
+
+
+def ring_peers(j: int, d_cp: int, w: int) -> RingPeers:
+    n = d_cp // w
+    ring, pos = divmod(j, w)
+
+    def idx(r, p):
+        return (r % n) * w + (p % w)
+
+    return RingPeers(idx(ring, pos + 1), idx(ring, pos - 1), idx(ring + 1, pos), idx(ring - 1, pos),
+                     idx(ring + 1, pos + 1), idx(ring - 1, pos - 1))
+
+
+def dkv_hop(step: int, d_cp: int, w: int) -> str:
+    """Hop of the backward dK/dV accumulator after step `step`: 'inner' while
+    the next step stays in the same outer step, else 'diag' (incl. home)."""
+    if step == d_cp - 1 or (step + 1) % w == 0:
+        return "diag"
+    return "inner"
+
+
+def check_dkv_route(schedule: RingSchedule) -> None:
+    """Prove the backward accumulator routing: the accumulator a rank forwards
+    after step s reaches exactly the rank that consumes the same chunk at step
+    s+1, and after the last step every accumulator lands at its owner."""
+    d_cp, w = schedule.d_cp, schedule.inner_ring
+    holder = {j: schedule.steps[j][0].source for j in range(d_cp)}  # rank -> chunk of its accumulator
+    seen = {c: [] for c in range(d_cp)}
+    for j in range(d_cp):
+        seen[holder[j]].append(j)
+    for s in range(d_cp):
+        kind = dkv_hop(s, d_cp, w)
+        nxt = {}
+        for j in range(d_cp):
+            p = ring_peers(j, d_cp, w)
+            to = p.inner_to if kind == "inner" else p.diag_to
+            nxt[to] = holder[j]
+        holder = nxt
+        if s + 1 < d_cp:
+            for j in range(d_cp):
+                want = schedule.steps[j][s + 1].source
+                if holder[j] != want:
+                    raise AssertionError(f"step {s + 1}: rank {j} holds dKV of {holder[j]}, consumes {want}")
+                seen[want].append(j)
+    if any(holder[j] != j for j in range(d_cp)):
+        raise AssertionError(f"home hop misroutes: {holder}")
+    for c, ranks in seen.items():
+        if sorted(ranks) != list(range(d_cp)):
+            raise AssertionError(f"chunk {c} accumulator visited {ranks}")
+
+
 def check_walk(schedule: RingSchedule) -> None:
     """Assert the hop patterns reproduce the consumption table exactly.
 
