@@ -69,6 +69,23 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t 
   return A2D_OK;
 }
 
+// fp32 [n2][n1][n0] tensor map, box {box0, box1, 1}, no swizzle (bulk reduce target).
+static int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n1, uint64_t n2,
+                            uint32_t box0, uint32_t box1) {
+  auto enc = get_encode();
+  if (!enc) return fail(A2D_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(A2D_EINVAL, "tensor base not 16-byte aligned");
+  cuuint64_t dims[3] = {n0, n1, n2};
+  cuuint64_t strides[2] = {n0 * 4, n0 * n1 * 4};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(A2D_ECUDA, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string((int)r) + ")");
+  return A2D_OK;
+}
+
 static int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -164,10 +181,11 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
   if (Tq > 0) {
     if ((rc = make_tmap_bf16_3d(&p.tm_q, q, D, Tq, H, D, Tq * D, 64))) return rc;
     if ((rc = make_tmap_bf16_3d(&p.tm_do, dout, D, Tq, H, D, Tq * D, 64))) return rc;
+    if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc, D, Tq, H, 128, 32))) return rc;
   }
   if ((rc = make_tmap_bf16_3d(&p.tm_k, k, D, Tk, H_kv, D, Tk * D, 128))) return rc;
   if ((rc = make_tmap_bf16_3d(&p.tm_v, v, D, Tk, H_kv, D, Tk * D, 128))) return rc;
-  if (Tq == 0) { p.tm_q = p.tm_k; p.tm_do = p.tm_k; }
+  if (Tq == 0) { p.tm_q = p.tm_k; p.tm_do = p.tm_k; p.tm_dq = p.tm_k; }
   p.q_pos = q_pos;
   p.k_pos = k_pos;
   p.q_bounds = reinterpret_cast<const int2*>(q_bounds64);

@@ -9,20 +9,23 @@
 // GQA: the CTA walks every query head of its KV head's group, so dK/dV sum
 // over the G sharing heads inside TMEM (ref oracle.py:149-151).
 //
-// One CTA = one 128-key tile of one KV head; it streams 64-row query tiles.
-// Everything is computed key-major ("transposed") so that the key tile owns
-// the 128 TMEM lanes:
-//   S^T  = K Q^T      (M=128 keys, N=64 q, K=d)   TMEM region b
-//   dP^T = V dO^T                                  TMEM region b
-//   dQ^T = K^T dS^T   (M=d, N=64 q, K=128 keys)    TMEM region b (over S^T)
+// One CTA = one 128-key tile of one KV head; it streams the live 64-row query
+// tiles (a compacted list built once in shared memory: causal-dead tiles cost
+// nothing). Everything is key-major so the key tile owns the 128 TMEM lanes:
+//   S^T  = K Q^T      (M=128 keys, N=64 q, K=d)   TMEM region b, cols [0,64)
+//   dP^T = V dO^T                                  TMEM region b, cols [64,128)
+//   P^T (bf16) is written back inside each warpgroup's own S^T columns
+//   (queries 0-31 -> cols [0,16), 32-63 -> cols [32,48)) and feeds dV as a
+//   TMEM operand; dQ^T = K^T dS^T (M=d, N=64 q, K=128 keys) then lands in
+//   cols [0,64)
 //   dV  += P^T dO     (M=128 keys, N=d, K=64 q)    TMEM [256,384)
 //   dK  += dS^T Q                                  TMEM [384,512)
-// P^T and dS^T go through shared memory in the SW128 K-major layout; the same
-// bytes are the MN-major B operand of dQ^T, so one copy serves both GEMMs.
+// dS^T goes through shared memory in the SW128 K-major layout; the same bytes
+// are the MN-major B operand of dQ^T, so one copy serves both GEMMs.
+// dQ^T is drained TMEM -> smem (fp32 [q][d]) -> TMA bulk tensor reduce-add
+// into dq_acc (the add happens in L2, one 16 KB op per warpgroup/iteration).
 // Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 two compute warpgroups that
-// split every 64-query iteration in halves: P and dS for their 32 query
-// columns, then the matching half of dQ^T drained with fp32 reductions into
-// dq_acc while the tensor core runs dV/dK.
+// split every 64-query iteration in halves (P, dS, dQ^T drain of 32 queries).
 #include "sm100.cuh"
 #include "kernels.h"
 
@@ -32,26 +35,31 @@ namespace bwd {
 constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 64;   // queries per iteration
 constexpr int D = 128;
-constexpr int QST = 2;   // Q/dO stages
+constexpr int QST = 3;   // Q/dO stages (TMA latency off the critical path)
 constexpr int kThreads = 384;
+constexpr int kMaxQTiles = 4096;                 // live-list capacity (Tq <= 256K per chunk)
+constexpr uint16_t kFullBit = 0x8000;
 // smem layout (bytes, from 1 KB aligned base)
 constexpr int kK = 0;
 constexpr int kV = kK + BK * D * 2;              // 32 KB each
 constexpr int kQ = kV + BK * D * 2;              // QST x 16 KB
 constexpr int kDO = kQ + QST * BQ * D * 2;       // QST x 16 KB
-constexpr int kP = kDO + QST * BQ * D * 2;       // 2 x 16 KB  (P^T, [key][q])
-constexpr int kDS = kP + 2 * BK * BQ * 2;        // 2 x 16 KB  (dS^T)
-constexpr int kStats = kDS + 2 * BK * BQ * 2;    // QST x (lse2[64], delta[64])
-constexpr int kEnd = kStats + QST * 2 * BQ * 4;
+constexpr int kDS = kDO + QST * BQ * D * 2;      // 16 KB  (dS^T, [key][q] SW128)
+constexpr int kDQ = kDS + BK * BQ * 2;           // 32 KB fp32 dQ staging [64 q][128 d]
+constexpr int kStats = kDQ + BQ * D * 4;         // QST x (lse2[64], delta[64])
+constexpr int kList = kStats + QST * 2 * BQ * 4; // live query tiles (int)
+constexpr int kEnd = kList + kMaxQTiles * 2;
 constexpr int kBytes = kEnd + 1024;
 }  // namespace bwd
 
 struct BwdBars {
   uint64_t kv_full;
   uint64_t qdo_full[bwd::QST], qdo_empty[bwd::QST];
-  uint64_t s_full[2], ds_full[2], dq_full[2], dq_empty[2], pds_free[2];
+  uint64_t s_full[2], ds_full[2], dq_full[2], dq_empty[2], ds_free;
   uint64_t dkv_full;
   uint32_t tmem_base;
+  int n_live;
+  int warp_cnt[12];
 };
 
 A2D_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -77,13 +85,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   const int Tq_pad = nqt * BQ;
   const int2 kb = p.k_bounds[kt];
   const bool causal = p.causal != 0;
-  const int n_iter_max = p.G * nqt;
-
-  // live(i): query tile qt of head g = i / nqt sees at least one key of this tile
-  auto live = [&](int qt) {
-    const int2 qb = p.q_bounds[qt];
-    return qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y);
-  };
+  uint16_t* live_list = reinterpret_cast<uint16_t*>(smem + kList);
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
@@ -93,58 +95,92 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       mbar_init(&bars.ds_full[b], 256);
       mbar_init(&bars.dq_full[b], 1);
       mbar_init(&bars.dq_empty[b], 256);
-      mbar_init(&bars.pds_free[b], 1);
     }
+    mbar_init(&bars.ds_free, 1);
     mbar_init(&bars.dkv_full, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(&bars.tmem_base);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.tm_q); tma_prefetch(&p.tm_k); tma_prefetch(&p.tm_v); tma_prefetch(&p.tm_do);
+    tma_prefetch(&p.tm_dq);
+  }
+  // ---- compacted list of live query tiles: every warp scans a contiguous
+  // range, counts, then writes its survivors at its prefix offset.
+  {
+    const int per_warp = (nqt + 11) / 12;
+    const int lo = warp * per_warp, hi = min(nqt, lo + per_warp);
+    int cnt = 0;
+    for (int base = lo; base < hi; base += 32) {
+      const int qt = base + lane;
+      bool lv = false;
+      if (qt < hi) {
+        const int2 qb = p.q_bounds[qt];
+        lv = qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y);
+      }
+      cnt += __popc(__ballot_sync(0xffffffffu, lv));
+    }
+    if (lane == 0) bars.warp_cnt[warp] = cnt;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < warp; ++w) off += bars.warp_cnt[w];
+    if (warp == 11 && lane == 0) bars.n_live = off + cnt;
+    for (int base = lo; base < hi; base += 32) {
+      const int qt = base + lane;
+      bool lv = false, full = false;
+      if (qt < hi) {
+        const int2 qb = p.q_bounds[qt];
+        lv = qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y);
+        full = !causal || kb.y <= qb.x;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, lv);
+      if (lv) live_list[off + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(qt | (full ? kFullBit : 0));
+      off += __popc(m);
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
+  const int n_live = bars.n_live;
+  const int n = n_live * p.G;  // iterations: (g, live tile) g-major
 
   if (warp == 0) {
     // -------------------------------------------------------------- producer
-    if (lane == 0) {
+    if (lane == 0 && n > 0) {
       mbar_expect_tx(&bars.kv_full, 2 * BK * D * 2);
       for (int c = 0; c < 2; ++c) {
         tma_load_3d(smem + kK + c * 16384, &p.tm_k, &bars.kv_full, c * 64, key0, hk);
         tma_load_3d(smem + kV + c * 16384, &p.tm_v, &bars.kv_full, c * 64, key0, hk);
       }
       int it = 0;
-      for (int i = 0; i < n_iter_max; ++i) {
-        const int g = i / nqt, qt = i % nqt;
-        if (!live(qt)) continue;
+      for (int g = 0; g < p.G; ++g) {
         const int h = hk * p.G + g;
-        const int qs = it % QST;
-        mbar_wait(&bars.qdo_empty[qs], ((it / QST) & 1) ^ 1);
-        mbar_expect_tx(&bars.qdo_full[qs], 2 * BQ * D * 2 + 2 * BQ * 4);
-        for (int c = 0; c < 2; ++c) {
-          tma_load_3d(smem + kQ + qs * BQ * D * 2 + c * 8192, &p.tm_q, &bars.qdo_full[qs], c * 64, qt * BQ, h);
-          tma_load_3d(smem + kDO + qs * BQ * D * 2 + c * 8192, &p.tm_do, &bars.qdo_full[qs], c * 64, qt * BQ, h);
+        for (int li = 0; li < n_live; ++li, ++it) {
+          const int qt = live_list[li] & (kFullBit - 1);
+          const int qs = it % QST;
+          mbar_wait(&bars.qdo_empty[qs], ((it / QST) & 1) ^ 1);
+          mbar_expect_tx(&bars.qdo_full[qs], 2 * BQ * D * 2 + 2 * BQ * 4);
+          for (int c = 0; c < 2; ++c) {
+            tma_load_3d(smem + kQ + qs * BQ * D * 2 + c * 8192, &p.tm_q, &bars.qdo_full[qs], c * 64, qt * BQ, h);
+            tma_load_3d(smem + kDO + qs * BQ * D * 2 + c * 8192, &p.tm_do, &bars.qdo_full[qs], c * 64, qt * BQ,
+                        h);
+          }
+          float* st = reinterpret_cast<float*>(smem + kStats) + qs * 2 * BQ;
+          bulk_g2s(st, p.lse2 + (size_t)h * Tq_pad + qt * BQ, BQ * 4, &bars.qdo_full[qs]);
+          bulk_g2s(st + BQ, p.delta + (size_t)h * Tq_pad + qt * BQ, BQ * 4, &bars.qdo_full[qs]);
         }
-        float* st = reinterpret_cast<float*>(smem + kStats) + qs * 2 * BQ;
-        bulk_g2s(st, p.lse2 + (size_t)h * Tq_pad + qt * BQ, BQ * 4, &bars.qdo_full[qs]);
-        bulk_g2s(st + BQ, p.delta + (size_t)h * Tq_pad + qt * BQ, BQ * 4, &bars.qdo_full[qs]);
-        ++it;
       }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      int n = 0;
-      for (int qt = 0; qt < nqt; ++qt) n += live(qt) ? 1 : 0;
-      n *= p.G;
+    if (lane == 0 && n > 0) {
       constexpr uint32_t id_s = idesc_bf16(BK, BQ, false, false);   // S^T, dP^T
       constexpr uint32_t id_kv = idesc_bf16(BK, D, false, true);    // dV, dK
       constexpr uint32_t id_dq = idesc_bf16(D, BQ, true, true);     // dQ^T
       const uint32_t sK = smem_u32(smem + kK), sV = smem_u32(smem + kV);
       const uint32_t sQ = smem_u32(smem + kQ), sDO = smem_u32(smem + kDO);
-      const uint32_t sP = smem_u32(smem + kP), sDS = smem_u32(smem + kDS);
+      const uint32_t sDS = smem_u32(smem + kDS);
       const uint32_t tDV = tmem + 256, tDK = tmem + 384;
       auto issue_s = [&](int i) {  // S^T_i and dP^T_i into region i&1
         const int b = i & 1, qs = i % QST;
@@ -157,45 +193,44 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
           umma_ss(tDP, sdesc_sw128(sV + ka, 16, 1024), sdesc_sw128(sDO + kq, 16, 1024), id_s, k > 0);
         }
       };
-      if (n > 0) {
-        mbar_wait(&bars.kv_full, 0);
-        for (int i = 0; i < 2 && i < n; ++i) {
-          mbar_wait(&bars.qdo_full[i % QST], (i / QST) & 1);
-          tc_fence_after();
-          issue_s(i);
-          umma_commit(&bars.s_full[i & 1]);
-        }
-        for (int i = 0; i < n; ++i) {
-          const int b = i & 1, qs = i % QST;
-          mbar_wait(&bars.ds_full[b], (i >> 1) & 1);
-          tc_fence_after();
-          // dQ^T_i = K^T dS^T_i -> region b columns [0, 64)
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_ss(tmem + b * 128, sdesc_sw128(sK + k * 2048, 16384, 1024),
-                    sdesc_sw128(sDS + b * 16384 + k * 2048, 8192, 1024), id_dq, k > 0);
-          umma_commit(&bars.dq_full[b]);
-          // dV += P^T dO ; dK += dS^T Q
-#pragma unroll
-          for (int k = 0; k < BQ / 16; ++k) {
-            const uint32_t kmn = qs * BQ * D * 2 + k * 2048;
-            umma_ss(tDV, sdesc_sw128(sP + b * 16384 + k * 32, 16, 1024), sdesc_sw128(sDO + kmn, 8192, 1024),
-                    id_kv, (i > 0 || k > 0) ? 1u : 0u);
-            umma_ss(tDK, sdesc_sw128(sDS + b * 16384 + k * 32, 16, 1024), sdesc_sw128(sQ + kmn, 8192, 1024),
-                    id_kv, (i > 0 || k > 0) ? 1u : 0u);
-          }
-          umma_commit(&bars.pds_free[b]);
-          umma_commit(&bars.qdo_empty[qs]);
-          if (i + 2 < n) {
-            mbar_wait(&bars.dq_empty[b], (i >> 1) & 1);
-            mbar_wait(&bars.qdo_full[(i + 2) % QST], ((i + 2) / QST) & 1);
-            tc_fence_after();
-            issue_s(i + 2);
-            umma_commit(&bars.s_full[b]);
-          }
-        }
-        umma_commit(&bars.dkv_full);
+      mbar_wait(&bars.kv_full, 0);
+      for (int i = 0; i < 2 && i < n; ++i) {
+        mbar_wait(&bars.qdo_full[i % QST], (i / QST) & 1);
+        tc_fence_after();
+        issue_s(i);
+        umma_commit(&bars.s_full[i & 1]);
       }
+      for (int i = 0; i < n; ++i) {
+        const int b = i & 1, qs = i % QST;
+        mbar_wait(&bars.ds_full[b], (i >> 1) & 1);
+        tc_fence_after();
+        // dV += P^T dO   (P^T from TMEM region b: queries 16k.. at col (k/2)*32 + (k%2)*8)
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k)
+          umma_ts(tDV, tmem + b * 128 + (k / 2) * 32 + (k % 2) * 8, sdesc_sw128(sDO + qs * BQ * D * 2 + k * 2048, 8192, 1024), id_kv,
+                  (i > 0 || k > 0) ? 1u : 0u);
+        // dQ^T_i = K^T dS^T_i -> region b cols [0,64) (after dV read P^T: in-order)
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_ss(tmem + b * 128, sdesc_sw128(sK + k * 2048, 16384, 1024),
+                  sdesc_sw128(sDS + k * 2048, 8192, 1024), id_dq, k > 0);
+        umma_commit(&bars.dq_full[b]);
+        // dK += dS^T Q
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k)
+          umma_ss(tDK, sdesc_sw128(sDS + k * 32, 16, 1024),
+                  sdesc_sw128(sQ + qs * BQ * D * 2 + k * 2048, 8192, 1024), id_kv, (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&bars.ds_free);
+        umma_commit(&bars.qdo_empty[qs]);
+        if (i + 2 < n) {
+          mbar_wait(&bars.dq_empty[b], (i >> 1) & 1);
+          mbar_wait(&bars.qdo_full[(i + 2) % QST], ((i + 2) / QST) & 1);
+          tc_fence_after();
+          issue_s(i + 2);
+          umma_commit(&bars.s_full[b]);
+        }
+      }
+      umma_commit(&bars.dkv_full);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ compute warpgroups
@@ -211,85 +246,88 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const float sl2 = p.scale_log2, scale = p.scale;
     const int c0 = hq * 32;
+    float* dq_stage = reinterpret_cast<float*>(smem + kDQ) + c0 * D;  // [32 q][128 d]
+    const bool leader = (warp % 4 == 0) && lane == 0;
     int it = 0;
-    for (int i = 0; i < n_iter_max; ++i) {
-      const int g = i / nqt, qt = i % nqt;
-      const int2 qb = p.q_bounds[qt];
-      if (!(qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y))) continue;
-      const bool full = !causal || kb.y <= qb.x;
+    for (int g = 0; g < p.G; ++g) {
       const int h = hk * p.G + g;
-      const int b = it & 1, qs = it % QST;
-      int qpos[32];
-      if (!full) {
+      for (int li = 0; li < n_live; ++li, ++it) {
+        const int ent = live_list[li];
+        const int qt = ent & (kFullBit - 1);
+        const bool full = (ent & kFullBit) != 0;
+        const int b = it & 1, qs = it % QST;
+        int qpos[32];
+        if (!full) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int q = qt * BQ + c0 + c;
-          qpos[c] = q < p.Tq ? __ldg(p.q_pos + q) : INT_MIN;
+          for (int c = 0; c < 32; ++c) {
+            const int q = qt * BQ + c0 + c;
+            qpos[c] = q < p.Tq ? __ldg(p.q_pos + q) : INT_MIN;
+          }
+        }
+        mbar_wait(&bars.qdo_full[qs], (it / QST) & 1);  // stats landed with the TMA stage
+        const float4* st4 = reinterpret_cast<const float4*>(smem + kStats + qs * 2 * BQ * 4);
+        mbar_wait(&bars.s_full[b], (it >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tmem + lane_base + b * 128 + c0, sr);
+        tmem_ld32(tmem + lane_base + b * 128 + 64 + c0, dr);
+        tmem_ld_wait();
+        uint32_t pw[16], dw[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const float4 l4 = st4[(c0 + c) / 4];
+          const float4 d4 = st4[(BQ + c0 + c) / 4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+          const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pv[4], dsv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            bool keep = key_ok;
+            if (!full) keep = keep && kpos <= qpos[c + e];
+            const float pr = keep ? ex2(fmaf(__uint_as_float(sr[c + e]), sl2, -lv[e])) : 0.f;
+            pv[e] = pr;
+            dsv[e] = pr * scale * (__uint_as_float(dr[c + e]) - dv4[e]);
+          }
+          pw[c / 2] = pack_bf16(pv[0], pv[1]);
+          pw[c / 2 + 1] = pack_bf16(pv[2], pv[3]);
+          dw[c / 2] = pack_bf16(dsv[0], dsv[1]);
+          dw[c / 2 + 1] = pack_bf16(dsv[2], dsv[3]);
+        }
+        // P^T (bf16 pairs) inside this warpgroup's own S^T columns: [c0, c0+16)
+        tmem_st16(tmem + lane_base + b * 128 + c0, pw);
+        if (it >= 1) mbar_wait(&bars.ds_free, (it - 1) & 1);  // dK/dQ^T of it-1 done reading dS
+        uint8_t* dsrow = smem + kDS;
+#pragma unroll
+        for (int c8 = 0; c8 < 4; ++c8)
+          *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, hq * 4 + c8)) =
+              make_uint4(dw[4 * c8], dw[4 * c8 + 1], dw[4 * c8 + 2], dw[4 * c8 + 3]);
+        fence_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars.ds_full[b]);
+        // ---- dQ^T drain: TMEM -> smem [q][d] fp32 -> bulk reduce-add
+        mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_base + b * 128 + c0, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bars.dq_empty[b]);
+        if (leader) bulk_wait_read0();           // previous reduce finished reading the stage
+        named_bar_sync(1 + hq, 128);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dq_stage[c * D + r] = __uint_as_float(v[c]);
+        fence_async_smem();
+        named_bar_sync(1 + hq, 128);
+        if (leader) {
+          tma_reduce_add_3d(&p.tm_dq, dq_stage, 0, qt * BQ + c0, h);
+          bulk_commit();
         }
       }
-      mbar_wait(&bars.qdo_full[qs], (it / QST) & 1);  // stats landed with the TMA stage
-      const float4* st4 = reinterpret_cast<const float4*>(smem + kStats + qs * 2 * BQ * 4);
-      mbar_wait(&bars.s_full[b], (it >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[32], dr[32];
-      tmem_ld32(tmem + lane_base + b * 128 + c0, sr);
-      tmem_ld32(tmem + lane_base + b * 128 + 64 + c0, dr);
-      tmem_ld_wait();
-      uint32_t pw[16], dw[16];
-#pragma unroll
-      for (int c = 0; c < 32; c += 4) {
-        const float4 l4 = st4[(c0 + c) / 4];
-        const float4 d4 = st4[(BQ + c0 + c) / 4];
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-        const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-        float pv[4], dsv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          bool keep = key_ok;
-          if (!full) keep = keep && kpos <= qpos[c + e];
-          const float pr = keep ? ex2(fmaf(__uint_as_float(sr[c + e]), sl2, -lv[e])) : 0.f;
-          pv[e] = pr;
-          dsv[e] = pr * scale * (__uint_as_float(dr[c + e]) - dv4[e]);
-        }
-        pw[c / 2] = pack_bf16(pv[0], pv[1]);
-        pw[c / 2 + 1] = pack_bf16(pv[2], pv[3]);
-        dw[c / 2] = pack_bf16(dsv[0], dsv[1]);
-        dw[c / 2 + 1] = pack_bf16(dsv[2], dsv[3]);
-      }
-      if (it >= 2) mbar_wait(&bars.pds_free[b], ((it - 2) >> 1) & 1);  // P/dS smem b reusable
-      uint8_t* prow = smem + kP + b * 16384;
-      uint8_t* dsrow = smem + kDS + b * 16384;
-#pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
-        *reinterpret_cast<uint4*>(prow + sw128_offset(r, hq * 4 + c8)) =
-            make_uint4(pw[4 * c8], pw[4 * c8 + 1], pw[4 * c8 + 2], pw[4 * c8 + 3]);
-        *reinterpret_cast<uint4*>(dsrow + sw128_offset(r, hq * 4 + c8)) =
-            make_uint4(dw[4 * c8], dw[4 * c8 + 1], dw[4 * c8 + 2], dw[4 * c8 + 3]);
-      }
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(&bars.ds_full[b]);
-      // drain this iteration's dQ^T (issued by the MMA warp right after ds_full)
-      mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
-      tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tmem + lane_base + b * 128 + c0, v);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&bars.dq_empty[b]);
-      const int q0 = qt * BQ + c0;
-      float* dst = p.dq_acc + ((size_t)h * p.Tq + q0) * D + r;
-      if (q0 + 32 <= p.Tq) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) atomicAdd(dst + (size_t)c * D, __uint_as_float(v[c]));
-      } else {
-        for (int c = 0; c < 32; ++c)
-          if (q0 + c < p.Tq) atomicAdd(dst + (size_t)c * D, __uint_as_float(v[c]));
-      }
-      ++it;
     }
+    if (leader) bulk_wait0();
     // ------------------------------------------------ dV (hq=0) / dK (hq=1) epilogue
-    if (it > 0) {
+    if (n > 0) {
       mbar_wait(&bars.dkv_full, 0);
       tc_fence_after();
     }
@@ -297,7 +335,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
       uint32_t rr[32];
-      if (it > 0) {
+      if (n > 0) {
         tmem_ld32(tmem + lane_base + 256 + hq * 128 + c * 32, rr);
         tmem_ld_wait();
       } else {
@@ -307,14 +345,14 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       if (key_ok) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          float4 v = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]), __uint_as_float(rr[j + 2]),
-                                 __uint_as_float(rr[j + 3]));
+          float4 val = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]), __uint_as_float(rr[j + 2]),
+                                   __uint_as_float(rr[j + 3]));
           float4* d4 = reinterpret_cast<float4*>(dst + c * 32 + j);
           if (p.accumulate_kv) {
             const float4 o = *d4;
-            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            val.x += o.x; val.y += o.y; val.z += o.z; val.w += o.w;
           }
-          *d4 = v;
+          *d4 = val;
         }
       }
     }
@@ -328,6 +366,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
 cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
   if (head_dim != 128) return cudaErrorInvalidValue;
   if (p.Tk <= 0 || p.Hkv <= 0) return cudaSuccess;
+  if ((p.Tq + bwd::BQ - 1) / bwd::BQ > bwd::kMaxQTiles) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd::kBytes);
   if (e != cudaSuccess) return e;
   dim3 grid((p.Tk + bwd::BK - 1) / bwd::BK, p.Hkv);

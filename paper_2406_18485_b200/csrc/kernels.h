@@ -31,6 +31,7 @@ cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s);
 // D = rowsum(dO * O) of the query chunk.
 struct BwdParams {
   CUtensorMap tm_q, tm_k, tm_v, tm_do;  // box {64,64,1} for q/do, {64,128,1} for k/v
+  CUtensorMap tm_dq;                    // fp32 dq_acc [H][Tq][128], box {128,32,1}, no swizzle
   const int* q_pos;
   const int* k_pos;
   const int2* q_bounds;   // per 64-row query tile
