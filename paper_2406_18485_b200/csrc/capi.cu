@@ -181,7 +181,7 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
   if (Tq > 0) {
     if ((rc = make_tmap_bf16_3d(&p.tm_q, q, D, Tq, H, D, Tq * D, 64))) return rc;
     if ((rc = make_tmap_bf16_3d(&p.tm_do, dout, D, Tq, H, D, Tq * D, 64))) return rc;
-    if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc, D, Tq, H, 128, 32))) return rc;
+    if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc, D, Tq, H, 128, 64))) return rc;
   }
   if ((rc = make_tmap_bf16_3d(&p.tm_k, k, D, Tk, H_kv, D, Tk * D, 128))) return rc;
   if ((rc = make_tmap_bf16_3d(&p.tm_v, v, D, Tk, H_kv, D, Tk * D, 128))) return rc;

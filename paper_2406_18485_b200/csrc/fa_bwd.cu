@@ -23,9 +23,9 @@
 // dS^T goes through shared memory in the SW128 K-major layout; the same bytes
 // are the MN-major B operand of dQ^T, so one copy serves both GEMMs.
 // dQ^T is drained TMEM -> smem (fp32 [q][d]) -> TMA bulk tensor reduce-add
-// into dq_acc (the add happens in L2, one 16 KB op per warpgroup/iteration).
-// Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 two compute warpgroups that
-// split every 64-query iteration in halves (P, dS, dQ^T drain of 32 queries).
+// into dq_acc (the add happens in L2, one 32 KB op per iteration).
+// Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 two P/dS warpgroups that split
+// every 64-query iteration in halves, 12-15 the dQ^T drain warpgroup.
 #include "sm100.cuh"
 #include "kernels.h"
 
@@ -36,7 +36,7 @@ constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 64;   // queries per iteration
 constexpr int D = 128;
 constexpr int QST = 3;   // Q/dO stages (TMA latency off the critical path)
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kMaxQTiles = 4096;                 // live-list capacity (Tq <= 256K per chunk)
 constexpr uint16_t kFullBit = 0x8000;
 // smem layout (bytes, from 1 KB aligned base)
@@ -59,7 +59,7 @@ struct BwdBars {
   uint64_t dkv_full;
   uint32_t tmem_base;
   int n_live;
-  int warp_cnt[12];
+  int warp_cnt[16];
 };
 
 A2D_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       mbar_init(&bars.s_full[b], 1);
       mbar_init(&bars.ds_full[b], 256);
       mbar_init(&bars.dq_full[b], 1);
-      mbar_init(&bars.dq_empty[b], 256);
+      mbar_init(&bars.dq_empty[b], 128);
     }
     mbar_init(&bars.ds_free, 1);
     mbar_init(&bars.dkv_full, 1);
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   // ---- compacted list of live query tiles: every warp scans a contiguous
   // range, counts, then writes its survivors at its prefix offset.
   {
-    const int per_warp = (nqt + 11) / 12;
+    const int per_warp = (nqt + 15) / 16;
     const int lo = warp * per_warp, hi = min(nqt, lo + per_warp);
     int cnt = 0;
     for (int base = lo; base < hi; base += 32) {
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     __syncthreads();
     int off = 0;
     for (int w = 0; w < warp; ++w) off += bars.warp_cnt[w];
-    if (warp == 11 && lane == 0) bars.n_live = off + cnt;
+    if (warp == 15 && lane == 0) bars.n_live = off + cnt;
     for (int base = lo; base < hi; base += 32) {
       const int qt = base + lane;
       bool lv = false, full = false;
@@ -232,11 +232,49 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       }
       umma_commit(&bars.dkv_full);
     }
+  } else if (warp >= 12) {
+    // ------------------------------------------------ dQ^T drain warpgroup
+    // TMEM lane = feature d; 64 query columns -> smem fp32 [q][d] -> one
+    // 32 KB TMA bulk reduce-add into dq_acc per iteration. Runs concurrently
+    // with the P/dS warpgroups, off their critical path.
+    const int wq = warp % 4;
+    const int d = wq * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    float* dq_stage = reinterpret_cast<float*>(smem + kDQ);  // [64 q][128 d]
+    const bool leader = warp == 12 && lane == 0;
+    int it = 0;
+    for (int g = 0; g < p.G; ++g) {
+      const int h = hk * p.G + g;
+      for (int li = 0; li < n_live; ++li, ++it) {
+        const int qt = live_list[li] & (kFullBit - 1);
+        const int b = it & 1;
+        mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld32(tmem + lane_base + b * 128, v0);
+        tmem_ld32(tmem + lane_base + b * 128 + 32, v1);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bars.dq_empty[b]);
+        if (leader) bulk_wait_read0();  // previous reduce finished reading the stage
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dq_stage[c * D + d] = __uint_as_float(v0[c]);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dq_stage[(c + 32) * D + d] = __uint_as_float(v1[c]);
+        fence_async_smem();
+        named_bar_sync(1, 128);
+        if (leader) {
+          tma_reduce_add_3d(&p.tm_dq, dq_stage, 0, qt * BQ, h);
+          bulk_commit();
+        }
+      }
+    }
+    if (leader) bulk_wait0();
   } else if (warp >= 4) {
-    // ------------------------------------------------ compute warpgroups
+    // ------------------------------------------------ P/dS warpgroups
     // Both warpgroups cover all 128 key rows (TMEM lanes); warpgroup hq owns
-    // query columns [32*hq, 32*hq+32) of every iteration, for P/dS and for
-    // the dQ^T drain (where the TMEM lane is the feature index d).
+    // query columns [32*hq, 32*hq+32) of every iteration.
     const int hq = (warp - 4) / 4;
     const int wq = warp % 4;
     const int r = wq * 32 + lane;
@@ -246,24 +284,15 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const float sl2 = p.scale_log2, scale = p.scale;
     const int c0 = hq * 32;
-    float* dq_stage = reinterpret_cast<float*>(smem + kDQ) + c0 * D;  // [32 q][128 d]
-    const bool leader = (warp % 4 == 0) && lane == 0;
+    const int* qpos_base = p.q_pos;
+    const int Tq = p.Tq;
     int it = 0;
     for (int g = 0; g < p.G; ++g) {
-      const int h = hk * p.G + g;
       for (int li = 0; li < n_live; ++li, ++it) {
         const int ent = live_list[li];
         const int qt = ent & (kFullBit - 1);
         const bool full = (ent & kFullBit) != 0;
         const int b = it & 1, qs = it % QST;
-        int qpos[32];
-        if (!full) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int q = qt * BQ + c0 + c;
-            qpos[c] = q < p.Tq ? __ldg(p.q_pos + q) : INT_MIN;
-          }
-        }
         mbar_wait(&bars.qdo_full[qs], (it / QST) & 1);  // stats landed with the TMA stage
         const float4* st4 = reinterpret_cast<const float4*>(smem + kStats + qs * 2 * BQ * 4);
         mbar_wait(&bars.s_full[b], (it >> 1) & 1);
@@ -283,7 +312,10 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             bool keep = key_ok;
-            if (!full) keep = keep && kpos <= qpos[c + e];
+            if (!full) {
+              const int q = qt * BQ + c0 + c + e;
+              keep = keep && q < Tq && kpos <= __ldg(qpos_base + q);
+            }
             const float pr = keep ? ex2(fmaf(__uint_as_float(sr[c + e]), sl2, -lv[e])) : 0.f;
             pv[e] = pr;
             dsv[e] = pr * scale * (__uint_as_float(dr[c + e]) - dv4[e]);
@@ -305,27 +337,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars.ds_full[b]);
-        // ---- dQ^T drain: TMEM -> smem [q][d] fp32 -> bulk reduce-add
-        mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
-        tc_fence_after();
-        uint32_t v[32];
-        tmem_ld32(tmem + lane_base + b * 128 + c0, v);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&bars.dq_empty[b]);
-        if (leader) bulk_wait_read0();           // previous reduce finished reading the stage
-        named_bar_sync(1 + hq, 128);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) dq_stage[c * D + r] = __uint_as_float(v[c]);
-        fence_async_smem();
-        named_bar_sync(1 + hq, 128);
-        if (leader) {
-          tma_reduce_add_3d(&p.tm_dq, dq_stage, 0, qt * BQ + c0, h);
-          bulk_commit();
-        }
       }
     }
-    if (leader) bulk_wait0();
     // ------------------------------------------------ dV (hq=0) / dK (hq=1) epilogue
     if (n > 0) {
       mbar_wait(&bars.dkv_full, 0);
