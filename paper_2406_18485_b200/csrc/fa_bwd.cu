@@ -4,7 +4,7 @@
 // FINAL softmax statistics of the query rows (global LSE, and
 // delta = rowsum(dO * O) = the reference's row = sum(dP * P), oracle.py:145):
 //   P   = exp(S - LSE)               dP = dO V^T
-//   dS  = P * (dP - delta) / sqrt(d)
+//   dS  = P * (dP - delta) / sqrt(d)   (the 1/sqrt(d) is applied after the GEMMs)
 //   dV += P^T dO    dK += dS^T Q    dQ += dS K
 // GQA: the CTA walks every query head of its KV head's group, so dK/dV sum
 // over the G sharing heads inside TMEM (ref oracle.py:149-151).
@@ -144,6 +144,15 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   const uint32_t tmem = bars.tmem_base;
   const int n_live = bars.n_live;
   const int n = n_live * p.G;  // iterations: (g, live tile) g-major
+  // register budget: TMA/MMA warpgroup and drain warpgroup give registers to
+  // the two P/dS warpgroups (80*128 + 96*128 + 2*152*128 <= 64K)
+  if (warp < 4) {
+    regs_dec<80>();
+  } else if (warp >= 12) {
+    regs_dec<96>();
+  } else {
+    regs_inc<152>();
+  }
 
   if (warp == 0) {
     // -------------------------------------------------------------- producer
@@ -242,6 +251,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     float* dq_stage = reinterpret_cast<float*>(smem + kDQ);  // [64 q][128 d]
     const bool leader = warp == 12 && lane == 0;
+    const float scale = p.scale;
     int it = 0;
     for (int g = 0; g < p.G; ++g) {
       const int h = hk * p.G + g;
@@ -259,9 +269,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         if (leader) bulk_wait_read0();  // previous reduce finished reading the stage
         named_bar_sync(1, 128);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dq_stage[c * D + d] = __uint_as_float(v0[c]);
+        for (int c = 0; c < 32; ++c) dq_stage[c * D + d] = __uint_as_float(v0[c]) * scale;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dq_stage[(c + 32) * D + d] = __uint_as_float(v1[c]);
+        for (int c = 0; c < 32; ++c) dq_stage[(c + 32) * D + d] = __uint_as_float(v1[c]) * scale;
         fence_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     const bool key_ok = key < p.Tk;
     const int kpos = key_ok ? p.k_pos[key] : INT_MAX;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const float sl2 = p.scale_log2, scale = p.scale;
+    const float sl2 = p.scale_log2;
     const int c0 = hq * 32;
     const int* qpos_base = p.q_pos;
     const int Tq = p.Tq;
@@ -302,28 +312,49 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tmem_ld32(tmem + lane_base + b * 128 + 64 + c0, dr);
         tmem_ld_wait();
         uint32_t pw[16], dw[16];
+        // dS is kept unscaled here (dS' = P*(dP-delta)); 1/sqrt(d) is applied in
+        // the dQ drain and the dK epilogue. Rows/keys past the chunk end need no
+        // mask: K/V rows there are zero-filled (their dS feeds dQ through zero
+        // K rows, their dK/dV rows are not stored) and padded query columns
+        // have lse2 = +inf (P = 0).
+        if (full) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 4) {
-          const float4 l4 = st4[(c0 + c) / 4];
-          const float4 d4 = st4[(BQ + c0 + c) / 4];
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-          const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-          float pv[4], dsv[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            bool keep = key_ok;
-            if (!full) {
-              const int q = qt * BQ + c0 + c + e;
-              keep = keep && q < Tq && kpos <= __ldg(qpos_base + q);
-            }
-            const float pr = keep ? ex2(fmaf(__uint_as_float(sr[c + e]), sl2, -lv[e])) : 0.f;
-            pv[e] = pr;
-            dsv[e] = pr * scale * (__uint_as_float(dr[c + e]) - dv4[e]);
+          for (int c = 0; c < 32; c += 4) {
+            const float4 l4 = st4[(c0 + c) / 4];
+            const float4 d4 = st4[(BQ + c0 + c) / 4];
+            const float p0 = ex2(fmaf(__uint_as_float(sr[c + 0]), sl2, -l4.x));
+            const float p1 = ex2(fmaf(__uint_as_float(sr[c + 1]), sl2, -l4.y));
+            const float p2 = ex2(fmaf(__uint_as_float(sr[c + 2]), sl2, -l4.z));
+            const float p3 = ex2(fmaf(__uint_as_float(sr[c + 3]), sl2, -l4.w));
+            pw[c / 2] = pack_bf16(p0, p1);
+            pw[c / 2 + 1] = pack_bf16(p2, p3);
+            dw[c / 2] = pack_bf16(p0 * (__uint_as_float(dr[c + 0]) - d4.x), p1 * (__uint_as_float(dr[c + 1]) - d4.y));
+            dw[c / 2 + 1] =
+                pack_bf16(p2 * (__uint_as_float(dr[c + 2]) - d4.z), p3 * (__uint_as_float(dr[c + 3]) - d4.w));
           }
-          pw[c / 2] = pack_bf16(pv[0], pv[1]);
-          pw[c / 2 + 1] = pack_bf16(pv[2], pv[3]);
-          dw[c / 2] = pack_bf16(dsv[0], dsv[1]);
-          dw[c / 2 + 1] = pack_bf16(dsv[2], dsv[3]);
+        } else {
+          const int qb0 = qt * BQ + c0;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            const float4 l4 = st4[(c0 + c) / 4];
+            const float4 d4 = st4[(BQ + c0 + c) / 4];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            const float dl[4] = {d4.x, d4.y, d4.z, d4.w};
+            float pv[4], dv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int q = qb0 + c + e;
+              const int qp = __ldg(qpos_base + min(q, Tq - 1));
+              const bool keep = key_ok && q < Tq && kpos <= qp;
+              const float pr = ex2(fmaf(__uint_as_float(sr[c + e]), sl2, -lv[e]));
+              pv[e] = keep ? pr : 0.f;
+              dv[e] = pv[e] * (__uint_as_float(dr[c + e]) - dl[e]);
+            }
+            pw[c / 2] = pack_bf16(pv[0], pv[1]);
+            pw[c / 2 + 1] = pack_bf16(pv[2], pv[3]);
+            dw[c / 2] = pack_bf16(dv[0], dv[1]);
+            dw[c / 2 + 1] = pack_bf16(dv[2], dv[3]);
+          }
         }
         // P^T (bf16 pairs) inside this warpgroup's own S^T columns: [c0, c0+16)
         tmem_st16(tmem + lane_base + b * 128 + c0, pw);
@@ -345,6 +376,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       tc_fence_after();
     }
     float* dst = (hq == 0 ? p.dv : p.dk) + ((size_t)hk * p.Tk + key) * D;
+    const float oscale = hq == 0 ? 1.f : p.scale;  // dK = (dS')^T Q / sqrt(d)
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
       uint32_t rr[32];
@@ -358,8 +390,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       if (key_ok) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          float4 val = make_float4(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]), __uint_as_float(rr[j + 2]),
-                                   __uint_as_float(rr[j + 3]));
+          float4 val = make_float4(__uint_as_float(rr[j]) * oscale, __uint_as_float(rr[j + 1]) * oscale,
+                                   __uint_as_float(rr[j + 2]) * oscale, __uint_as_float(rr[j + 3]) * oscale);
           float4* d4 = reinterpret_cast<float4*>(dst + c * 32 + j);
           if (p.accumulate_kv) {
             const float4 o = *d4;
