@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libattn2d_sm100.so")
+LIB_PATH = os.environ.get("A2D_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                        "libattn2d_sm100.so")
 
 _c_int, _c_i32, _c_i64, _c_f32, _vp = (ctypes.c_int, ctypes.c_int32, ctypes.c_int64,
                                       ctypes.c_float, ctypes.c_void_p)

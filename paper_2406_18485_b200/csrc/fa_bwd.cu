@@ -183,7 +183,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
-    if (lane == 0 && n > 0) {
+    // The whole (converged) warp runs this loop so descriptors are computed in
+    // uniform registers; an elected lane issues each group of tcgen05 ops.
+    if (n > 0) {
       constexpr uint32_t id_s = idesc_bf16(BK, BQ, false, false);   // S^T, dP^T
       constexpr uint32_t id_kv = idesc_bf16(BK, D, false, true);    // dV, dK
       constexpr uint32_t id_dq = idesc_bf16(D, BQ, true, true);     // dQ^T
@@ -191,55 +193,72 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       const uint32_t sQ = smem_u32(smem + kQ), sDO = smem_u32(smem + kDO);
       const uint32_t sDS = smem_u32(smem + kDS);
       const uint32_t tDV = tmem + 256, tDK = tmem + 384;
-      auto issue_s = [&](int i) {  // S^T_i and dP^T_i into region i&1
+      // loop-invariant descriptor bases (the start-address field advances by bytes>>4)
+      const uint64_t dK0 = sdesc_sw128(sK, 16, 1024), dV0 = sdesc_sw128(sV, 16, 1024);
+      const uint64_t dQ0 = sdesc_sw128(sQ, 16, 1024), dDO0 = sdesc_sw128(sDO, 16, 1024);
+      const uint64_t dKmn = sdesc_sw128(sK, 16384, 1024);  // K as MN-major A of dQ^T
+      const uint64_t dDSmn = sdesc_sw128(sDS, 8192, 1024);  // dS^T as MN-major B of dQ^T
+      const uint64_t dDSk = sdesc_sw128(sDS, 16, 1024);     // dS^T as K-major A of dK
+      const uint64_t dQmn = sdesc_sw128(sQ, 8192, 1024), dDOmn = sdesc_sw128(sDO, 8192, 1024);
+      auto issue_s = [&](int i) {  // S^T_i and dP^T_i into region i&1, then commit s_full
         const int b = i & 1, qs = i % QST;
         const uint32_t tS = tmem + b * 128, tDP = tmem + b * 128 + 64;
+        const uint64_t qoff = (uint64_t)((qs * BQ * D * 2) >> 4);
+        __syncwarp();
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t ka = (k / 4) * 16384 + (k % 4) * 32;
-          const uint32_t kq = qs * BQ * D * 2 + (k / 4) * 8192 + (k % 4) * 32;
-          umma_ss(tS, sdesc_sw128(sK + ka, 16, 1024), sdesc_sw128(sQ + kq, 16, 1024), id_s, k > 0);
-          umma_ss(tDP, sdesc_sw128(sV + ka, 16, 1024), sdesc_sw128(sDO + kq, 16, 1024), id_s, k > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t ka = (uint64_t)(((k / 4) * 16384 + (k % 4) * 32) >> 4);
+            const uint64_t kq = qoff + (uint64_t)(((k / 4) * 8192 + (k % 4) * 32) >> 4);
+            umma_ss(tS, dK0 + ka, dQ0 + kq, id_s, k > 0);
+            umma_ss(tDP, dV0 + ka, dDO0 + kq, id_s, k > 0);
+          }
+          umma_commit(&bars.s_full[b]);
         }
+        __syncwarp();
       };
       mbar_wait(&bars.kv_full, 0);
       for (int i = 0; i < 2 && i < n; ++i) {
         mbar_wait(&bars.qdo_full[i % QST], (i / QST) & 1);
         tc_fence_after();
         issue_s(i);
-        umma_commit(&bars.s_full[i & 1]);
       }
       for (int i = 0; i < n; ++i) {
         const int b = i & 1, qs = i % QST;
+        const uint64_t qoff = (uint64_t)((qs * BQ * D * 2) >> 4);
         mbar_wait(&bars.ds_full[b], (i >> 1) & 1);
         tc_fence_after();
-        // dV += P^T dO   (P^T from TMEM region b: queries 16k.. at col (k/2)*32 + (k%2)*8)
+        __syncwarp();
+        if (elect_one()) {
+          // dV += P^T dO   (P^T from TMEM region b: queries 16k.. at col (k/2)*32 + (k%2)*8)
 #pragma unroll
-        for (int k = 0; k < BQ / 16; ++k)
-          umma_ts(tDV, tmem + b * 128 + (k / 2) * 32 + (k % 2) * 8, sdesc_sw128(sDO + qs * BQ * D * 2 + k * 2048, 8192, 1024), id_kv,
-                  (i > 0 || k > 0) ? 1u : 0u);
-        // dQ^T_i = K^T dS^T_i -> region b cols [0,64) (after dV read P^T: in-order)
+          for (int k = 0; k < BQ / 16; ++k)
+            umma_ts(tDV, tmem + b * 128 + (k / 2) * 32 + (k % 2) * 8, dDOmn + qoff + (uint64_t)(k * 128), id_kv,
+                    (i > 0 || k > 0) ? 1u : 0u);
+          // dQ^T_i = K^T dS^T_i -> region b cols [0,64) (after dV read P^T: in-order)
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          umma_ss(tmem + b * 128, sdesc_sw128(sK + k * 2048, 16384, 1024),
-                  sdesc_sw128(sDS + k * 2048, 8192, 1024), id_dq, k > 0);
-        umma_commit(&bars.dq_full[b]);
-        // dK += dS^T Q
+          for (int k = 0; k < BK / 16; ++k)
+            umma_ss(tmem + b * 128, dKmn + (uint64_t)(k * 128), dDSmn + (uint64_t)(k * 128), id_dq, k > 0);
+          umma_commit(&bars.dq_full[b]);
+          // dK += dS^T Q
 #pragma unroll
-        for (int k = 0; k < BQ / 16; ++k)
-          umma_ss(tDK, sdesc_sw128(sDS + k * 32, 16, 1024),
-                  sdesc_sw128(sQ + qs * BQ * D * 2 + k * 2048, 8192, 1024), id_kv, (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&bars.ds_free);
-        umma_commit(&bars.qdo_empty[qs]);
+          for (int k = 0; k < BQ / 16; ++k)
+            umma_ss(tDK, dDSk + (uint64_t)(k * 2), dQmn + qoff + (uint64_t)(k * 128), id_kv,
+                    (i > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&bars.ds_free);
+          umma_commit(&bars.qdo_empty[qs]);
+        }
+        __syncwarp();
         if (i + 2 < n) {
           mbar_wait(&bars.dq_empty[b], (i >> 1) & 1);
           mbar_wait(&bars.qdo_full[(i + 2) % QST], ((i + 2) / QST) & 1);
           tc_fence_after();
           issue_s(i + 2);
-          umma_commit(&bars.s_full[b]);
         }
       }
-      umma_commit(&bars.dkv_full);
+      __syncwarp();
+      if (elect_one()) umma_commit(&bars.dkv_full);
+      __syncwarp();
     }
   } else if (warp >= 12) {
     // ------------------------------------------------ dQ^T drain warpgroup
