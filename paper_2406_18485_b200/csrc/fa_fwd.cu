@@ -12,7 +12,8 @@
 //
 // Structure (one CTA = 2 query tiles of 128 rows of one head, 12 warps):
 //   warp 0      TMA producer: Q once, then K/V tiles through 2-stage rings
-//   warp 1      MMA issuer (one thread): S_t = Q_t K^T into TMEM, O_t += P_t V
+//   warp 1      MMA issuer (converged warp, elected lane issues): S_t = Q_t K^T
+//               into TMEM, O_t += P_t V
 //   warp 2      TMEM allocator
 //   warps 4-7   softmax for query tile 0 (thread = row = TMEM lane)
 //   warps 8-11  softmax for query tile 1
@@ -32,6 +33,8 @@ constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 384;
 constexpr int KST = 2, VST = 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kMaxKTiles = 8192;           // live-list capacity (Tk <= 1M per chunk)
+constexpr uint16_t kMask0 = 0x4000, kMask1 = 0x8000, kIdx = 0x3fff;
 }  // namespace fwd
 
 template <int D>
@@ -40,7 +43,8 @@ struct FwdSmem {
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + 2 * kTileBytes;
   static constexpr int kV = kK + fwd::KST * kTileBytes;
-  static constexpr int kEnd = kV + fwd::VST * kTileBytes;
+  static constexpr int kList = kV + fwd::VST * kTileBytes;  // live KV tiles (uint16 + mask flags)
+  static constexpr int kEnd = kList + fwd::kMaxKTiles * 2;
   static constexpr int kBytes = kEnd + 1024;  // + alignment slack
 };
 
@@ -50,6 +54,8 @@ struct FwdBars {
   uint64_t v_full[fwd::VST], v_empty[fwd::VST];
   uint64_t s_full[2], p_full[2], o_full[2];
   uint32_t tmem_base;
+  int n_live;
+  int warp_cnt[12];
 };
 
 // Tile classification against one query tile's position range.
@@ -97,25 +103,59 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
     tma_prefetch(&p.tm_k);
     tma_prefetch(&p.tm_v);
   }
+  // ---- compacted list of live KV tiles for this CTA (causal-dead tiles
+  // never cost a loop iteration), with per-query-tile "needs mask" flags.
+  uint16_t* live_list = reinterpret_cast<uint16_t*>(smem + L::kList);
+  {
+    auto classify = [&](int j, bool& lv, uint16_t& ent) {
+      const int2 kb = p.k_bounds[j];
+      lv = tile_live(kb, qmax_cta, causal);
+      const bool tail = (j + 1) * BN > p.Tk;
+      const bool m0 = tail || (causal && !(qr0.x <= qr0.y && kb.y <= qr0.x));
+      const bool m1 = tail || (causal && !(qr1.x <= qr1.y && kb.y <= qr1.x));
+      ent = (uint16_t)(j | (m0 ? kMask0 : 0) | (m1 ? kMask1 : 0));
+    };
+    const int per_warp = (nkt + 11) / 12;
+    const int lo = warp * per_warp, hi = min(nkt, lo + per_warp);
+    int cnt = 0;
+    for (int base = lo; base < hi; base += 32) {
+      const int j = base + lane;
+      bool lv = false;
+      uint16_t ent = 0;
+      if (j < hi) classify(j, lv, ent);
+      cnt += __popc(__ballot_sync(0xffffffffu, lv));
+    }
+    if (lane == 0) bars.warp_cnt[warp] = cnt;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < warp; ++w) off += bars.warp_cnt[w];
+    if (warp == 11 && lane == 0) bars.n_live = off + cnt;
+    for (int base = lo; base < hi; base += 32) {
+      const int j = base + lane;
+      bool lv = false;
+      uint16_t ent = 0;
+      if (j < hi) classify(j, lv, ent);
+      const unsigned m = __ballot_sync(0xffffffffu, lv);
+      if (lv) live_list[off + __popc(m & ((1u << lane) - 1u))] = ent;
+      off += __popc(m);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
-
-  // number of live KV tiles for the CTA (same loop in every role)
-  auto live = [&](int j) { return tile_live(p.k_bounds[j], qmax_cta, causal); };
+  const int n = bars.n_live;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    if (lane == 0 && n > 0) {
       mbar_expect_tx(&bars.q_full, 2 * L::kTileBytes);
       for (int t = 0; t < 2; ++t)
         for (int c = 0; c < D / 64; ++c)
           tma_load_3d(smem + L::kQ + t * L::kTileBytes + c * 16384, &p.tm_q, &bars.q_full, c * 64,
                       q0 + t * BM, h);
-      int it = 0;
-      for (int j = 0; j < nkt; ++j) {
-        if (!live(j)) continue;
+      for (int it = 0; it < n; ++it) {
+        const int j = live_list[it] & kIdx;
         const int ks = it % KST, kph = (it / KST) & 1;
         mbar_wait(&bars.k_empty[ks], kph ^ 1);
         mbar_expect_tx(&bars.k_full[ks], L::kTileBytes);
@@ -128,60 +168,68 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         for (int c = 0; c < D / 64; ++c)
           tma_load_3d(smem + L::kV + vs * L::kTileBytes + c * 16384, &p.tm_v, &bars.v_full[vs], c * 64,
                       j * BN, hk);
-        ++it;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int n = 0;
-      for (int j = 0; j < nkt; ++j) n += live(j) ? 1 : 0;
+    // Converged warp (uniform-register descriptors); an elected lane issues.
+    if (n > 0) {
       constexpr uint32_t id_qk = idesc_bf16(BM, BN, false, false);
       constexpr uint32_t id_pv = idesc_bf16(BM, D, false, true);
-      const uint32_t sq = smem_u32(smem + L::kQ), sk = smem_u32(smem + L::kK), sv = smem_u32(smem + L::kV);
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const uint64_t dQ0 = sdesc_sw128(smem_u32(smem + L::kQ), 16, 1024);
+      const uint64_t dK0 = sdesc_sw128(smem_u32(smem + L::kK), 16, 1024);
+      const uint64_t dV0 = sdesc_sw128(smem_u32(smem + L::kV), 16384, 1024);
       auto issue_qk = [&](int t, int ks) {
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
-          umma_ss(tS[t], sdesc_sw128(sq + t * L::kTileBytes + off, 16, 1024),
-                  sdesc_sw128(sk + ks * L::kTileBytes + off, 16, 1024), id_qk, k > 0);
+          const uint64_t off = (uint64_t)(((k / 4) * 16384 + (k % 4) * 32) >> 4);
+          umma_ss(tS[t], dQ0 + (uint64_t)((t * L::kTileBytes) >> 4) + off,
+                  dK0 + (uint64_t)((ks * L::kTileBytes) >> 4) + off, id_qk, k > 0);
         }
       };
       auto issue_pv = [&](int t, int vs, bool acc) {
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k)
-          umma_ts(tO[t], tS[t] + k * 8, sdesc_sw128(sv + vs * L::kTileBytes + k * 2048, 16384, 1024), id_pv,
+          umma_ts(tO[t], tS[t] + k * 8, dV0 + (uint64_t)((vs * L::kTileBytes) >> 4) + (uint64_t)(k * 128), id_pv,
                   (acc || k > 0) ? 1u : 0u);
       };
-      if (n > 0) {
-        mbar_wait(&bars.q_full, 0);
-        mbar_wait(&bars.k_full[0], 0);
-        tc_fence_after();
+      mbar_wait(&bars.q_full, 0);
+      mbar_wait(&bars.k_full[0], 0);
+      tc_fence_after();
+      __syncwarp();
+      if (elect_one()) {
         issue_qk(0, 0);
         umma_commit(&bars.s_full[0]);
         issue_qk(1, 0);
         umma_commit(&bars.s_full[1]);
         umma_commit(&bars.k_empty[0]);
-        for (int it = 0; it < n; ++it) {
-          const int vs = it % VST;
-          mbar_wait(&bars.v_full[vs], (it / VST) & 1);
-          const bool more = it + 1 < n;
-          const int ks1 = (it + 1) % KST;
-          mbar_wait(&bars.p_full[0], it & 1);
-          tc_fence_after();
+      }
+      __syncwarp();
+      for (int it = 0; it < n; ++it) {
+        const int vs = it % VST;
+        mbar_wait(&bars.v_full[vs], (it / VST) & 1);
+        const bool more = it + 1 < n;
+        const int ks1 = (it + 1) % KST;
+        mbar_wait(&bars.p_full[0], it & 1);
+        if (more) mbar_wait(&bars.k_full[ks1], ((it + 1) / KST) & 1);
+        tc_fence_after();
+        __syncwarp();
+        if (elect_one()) {
           issue_pv(0, vs, it > 0);
           if (more) {
-            mbar_wait(&bars.k_full[ks1], ((it + 1) / KST) & 1);
-            tc_fence_after();
             issue_qk(0, ks1);
             umma_commit(&bars.s_full[0]);
           } else {
             umma_commit(&bars.o_full[0]);
           }
-          mbar_wait(&bars.p_full[1], it & 1);
-          tc_fence_after();
+        }
+        __syncwarp();
+        mbar_wait(&bars.p_full[1], it & 1);
+        tc_fence_after();
+        __syncwarp();
+        if (elect_one()) {
           issue_pv(1, vs, it > 0);
           umma_commit(&bars.v_empty[vs]);
           if (more) {
@@ -192,6 +240,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
             umma_commit(&bars.o_full[1]);
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -202,7 +251,6 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
     const int row = q0 + t * BM + row_in_tile;
     const bool row_ok = row < p.Tq;
     const int qpos = row_ok ? p.q_pos[row] : INT_MIN;
-    const int2 qr = t == 0 ? qr0 : qr1;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const uint32_t tS = tmem + lane_base + t * 128;
     const uint32_t tO = tmem + lane_base + 256 + t * 128;
@@ -210,14 +258,10 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
 
     float m_used = -INFINITY;  // running max, log2 units (scaled)
     float l_sum = 0.f;
-    int it = 0;
-    for (int j = 0; j < nkt; ++j) {
-      const int2 kb = p.k_bounds[j];
-      if (!tile_live(kb, qmax_cta, causal)) continue;
-      // tile status for this query tile: full (no mask), or masked
-      const bool tail = (j + 1) * BN > p.Tk;
-      const bool dead = causal && (qr.x > qr.y || kb.x > qr.y);
-      const bool full = !tail && !dead && (!causal || kb.y <= qr.x);
+    for (int it = 0; it < n; ++it) {
+      const int ent = live_list[it];
+      const int j = ent & kIdx;
+      const bool full = (ent & (t == 0 ? kMask0 : kMask1)) == 0;
 
       mbar_wait(&bars.s_full[t], it & 1);
       tc_fence_after();
@@ -232,14 +276,14 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
         }
       }
-      if (!full) {
-        const int* kp = p.k_pos + j * BN;
+      if (!full) {  // straddling / tail tile: per-element mask (branch-free)
+        const int tk1 = p.Tk - 1;
 #pragma unroll
         for (int c = 0; c < BN; ++c) {
           const int col = j * BN + c;
-          bool keep = col < p.Tk && !dead;
-          if (keep && causal) keep = __ldg(kp + c) <= qpos;
-          if (!keep) s[c] = -INFINITY;
+          const int kpos = __ldg(p.k_pos + min(col, tk1));
+          const bool keep = col <= tk1 && (!causal || kpos <= qpos);
+          s[c] = keep ? s[c] : -INFINITY;
         }
       }
       float mx = s[0];
@@ -286,10 +330,10 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars.p_full[t]);
-      ++it;
     }
 
     // ---------------------------------------------------------- epilogue
+    const int it = n;
     if (it > 0) {
       mbar_wait(&bars.o_full[t], 0);
       tc_fence_after();
@@ -362,6 +406,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
 
 template <int D>
 static cudaError_t launch_fwd_d(const FwdParams& p, cudaStream_t s) {
+  if ((p.Tk + fwd::BN - 1) / fwd::BN > fwd::kMaxKTiles) return cudaErrorInvalidValue;
   const int smem = FwdSmem<D>::kBytes;
   cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
