@@ -267,13 +267,19 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       tc_fence_after();
       float s[BN];
       {
-        uint32_t r[32];
+        // all four 32-column loads in flight before a single wait
+        uint32_t r0[32], r1[32], r2[32], r3[32];
+        tmem_ld32(tS + 0, r0);
+        tmem_ld32(tS + 32, r1);
+        tmem_ld32(tS + 64, r2);
+        tmem_ld32(tS + 96, r3);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          tmem_ld32(tS + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) {
+          s[i] = __uint_as_float(r0[i]);
+          s[32 + i] = __uint_as_float(r1[i]);
+          s[64 + i] = __uint_as_float(r2[i]);
+          s[96 + i] = __uint_as_float(r3[i]);
         }
       }
       if (!full) {  // straddling / tail tile: per-element mask (branch-free)
@@ -286,9 +292,16 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           s[c] = keep ? s[c] : -INFINITY;
         }
       }
-      float mx = s[0];
+      // row max: four independent chains (short dependency depth)
+      float mq[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-      for (int c = 1; c < BN; ++c) mx = fmaxf(mx, s[c]);
+      for (int c = 4; c < BN; c += 4) {
+        mq[0] = fmaxf(mq[0], s[c]);
+        mq[1] = fmaxf(mq[1], s[c + 1]);
+        mq[2] = fmaxf(mq[2], s[c + 2]);
+        mq[3] = fmaxf(mq[3], s[c + 3]);
+      }
+      const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
       const float m_tile = mx * sl2;  // -inf stays -inf (sl2 > 0)
       float alpha = 1.f;
       bool rescale = false;
@@ -298,16 +311,27 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         l_sum *= alpha;
       }
       const float neg_m = m_used == -INFINITY ? 0.f : -m_used;
-      float part[4] = {0.f, 0.f, 0.f, 0.f};
+      const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+      float2 part[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       uint32_t pk[BN / 2];
 #pragma unroll
       for (int c = 0; c < BN; c += 2) {
-        const float a = ex2(fmaf(s[c], sl2, neg_m));
-        const float b = ex2(fmaf(s[c + 1], sl2, neg_m));
-        part[(c / 2) & 3] += a + b;
-        pk[c / 2] = pack_bf16(a, b);
+        const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl2x2, nm2);
+        float2 e;
+        if (((c / 2) & 3) == 3) {  // one pair in four on the FMA pipe (MUFU relief)
+          e = ex2_poly2(x);
+        } else {
+          e.x = ex2(x.x);
+          e.y = ex2(x.y);
+        }
+        part[(c / 2) & 3] = __fadd2_rn(part[(c / 2) & 3], e);
+        pk[c / 2] = pack_bf16(e.x, e.y);
       }
-      l_sum += (part[0] + part[1]) + (part[2] + part[3]);
+      {
+        const float2 p01 = __fadd2_rn(part[0], part[1]), p23 = __fadd2_rn(part[2], part[3]);
+        const float2 pt = __fadd2_rn(p01, p23);
+        l_sum += pt.x + pt.y;
+      }
 #pragma unroll
       for (int c = 0; c < BN / 64; ++c) {
         uint32_t r[32];

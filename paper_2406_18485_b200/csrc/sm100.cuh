@@ -264,6 +264,21 @@ A2D_DEV float ex2_poly(float x) {
   const int n = __float_as_int(t) - 0x4B400000;
   return __int_as_float(__float_as_int(p) + (n << 23));
 }
+// Packed (f32x2) variant of ex2_poly: FADD2/FFMA2 on the FMA pipe.
+A2D_DEV float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(make_float2(0.054006658f, 0.054006658f), f, make_float2(0.24244328f, 0.24244328f));
+  p = __ffma2_rn(p, f, make_float2(0.69344431f, 0.69344431f));
+  p = __ffma2_rn(p, f, make_float2(0.99994266f, 0.99994266f));
+  // bits(t) << 23 == (round(x) + 0x4B400000) << 23 == round(x) << 23 (mod 2^32)
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 A2D_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
