@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       for (int g = 0; g < p.G; ++g) {
         const int h = hk * p.G + g;
         for (int li = 0; li < n_live; ++li, ++it) {
-          const int qt = live_list[li] & (kFullBit - 1);
+          const int qt = live_list[n_live - 1 - li] & (kFullBit - 1);
           const int qs = it % QST;
           mbar_wait(&bars.qdo_empty[qs], ((it / QST) & 1) ^ 1);
           mbar_expect_tx(&bars.qdo_full[qs], 2 * BQ * D * 2 + 2 * BQ * 4);
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     for (int g = 0; g < p.G; ++g) {
       const int h = hk * p.G + g;
       for (int li = 0; li < n_live; ++li, ++it) {
-        const int qt = live_list[li] & (kFullBit - 1);
+        const int qt = live_list[n_live - 1 - li] & (kFullBit - 1);
         const int b = it & 1;
         mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
         tc_fence_after();
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     int it = 0;
     for (int g = 0; g < p.G; ++g) {
       for (int li = 0; li < n_live; ++li, ++it) {
-        const int ent = live_list[li];
+        const int ent = live_list[n_live - 1 - li];
         const int qt = ent & (kFullBit - 1);
         const bool full = (ent & kFullBit) != 0;
         const int b = it & 1, qs = it % QST;
