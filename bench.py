@@ -255,6 +255,29 @@ def main():
     value = flops * a.steps / (t_ms * 1e-3) / 1e12
     ms_step = t_ms / a.steps
 
+    # ---------------- exposed communication: same step with every NCCL call
+    # skipped (kernels and buffers identical), max over ranks
+    exposed = None
+    if world > 1:
+        op.comm_enabled = False
+        step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(a.steps):
+            step()
+        c1.record()
+        torch.cuda.synchronize()
+        op.comm_enabled = True
+        tc = torch.tensor([c0.elapsed_time(c1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        t_comp = float(tc.item()) / a.steps
+        exposed = {"ms_per_step": ms_step, "compute_only_ms_per_step": t_comp,
+                   "exposed_ms": ms_step - t_comp, "frac": (ms_step - t_comp) / ms_step,
+                   "definition": "t_layer - t_layer(comm disabled, same kernels), max over ranks"}
+        dist.barrier()
+
     # ---------------- e2e through the same public API with host buffers
     e2e = None
     if not a.no_e2e:
@@ -329,7 +352,7 @@ def main():
             "tflops_per_gpu": per_gpu, "mfu": per_gpu / pk["bf16_tflops"],
             "mfu_sustained": per_gpu / pk["bf16_tflops_sustained"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk,
+            "clocks": clk, "exposed_comm": exposed,
         }
         print(json.dumps(line))
     dist.barrier()

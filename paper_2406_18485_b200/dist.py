@@ -146,6 +146,10 @@ class Attn2D:
         self.times = StepTimes()
         self.record_times = False
         self.saved = None
+        # False = "compute only": identical kernels and buffers, every NCCL call
+        # skipped (receive buffers keep pre-staged data). Only for measuring
+        # exposed communication (t_layer - t_compute_only, ref timeline.py:152).
+        self.comm_enabled = True
 
     # ------------------------------------------------------------ helpers
     def _buf(self, name: str, shape, dtype) -> torch.Tensor:
@@ -161,6 +165,8 @@ class Attn2D:
             self.times.mark(name)
 
     def _a2a(self, out: torch.Tensor, inp: torch.Tensor):
+        if not self.comm_enabled:
+            return
         dist.all_to_all_single(out, inp, group=self.hp_group)
 
     def _scatter_q(self, x: torch.Tensor, name: str, dk: int) -> torch.Tensor:
@@ -201,6 +207,8 @@ class Attn2D:
         return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
 
     def _p2p(self, group, send_t, to, recv_t, frm):
+        if not self.comm_enabled:
+            return None
         ops = [dist.P2POp(dist.isend, send_t, to, group), dist.P2POp(dist.irecv, recv_t, frm, group)]
         return dist.batch_isend_irecv(ops)
 
