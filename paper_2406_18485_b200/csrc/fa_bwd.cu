@@ -37,7 +37,7 @@ constexpr int BQ = 64;   // queries per iteration
 constexpr int D = 128;
 constexpr int QST = 3;   // Q/dO stages (TMA latency off the critical path)
 constexpr int kThreads = 512;
-constexpr int kMaxQTiles = 4096;                 // live-list capacity (Tq <= 256K per chunk)
+constexpr int kMaxQTiles = 8192;                 // live-list capacity (Tq <= 512K per chunk)
 constexpr uint16_t kFullBit = 0x8000;
 // smem layout (bytes, from 1 KB aligned base)
 constexpr int kK = 0;
