@@ -1,6 +1,7 @@
 // extern "C" boundary of libattn2d_sm100.so (declared in include/attn2d_sm100.h).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <mutex>
@@ -71,12 +72,12 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t 
 
 // fp32 [n2][n1][n0] tensor map, box {box0, box1, 1}, no swizzle (bulk reduce target).
 static int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n1, uint64_t n2,
-                            uint32_t box0, uint32_t box1) {
+                            uint64_t s2, uint32_t box0, uint32_t box1) {
   auto enc = get_encode();
   if (!enc) return fail(A2D_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(A2D_EINVAL, "tensor base not 16-byte aligned");
   cuuint64_t dims[3] = {n0, n1, n2};
-  cuuint64_t strides[2] = {n0 * 4, n0 * n1 * 4};
+  cuuint64_t strides[2] = {n0 * 4, s2 * 4};
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
@@ -176,35 +177,50 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
     return fail(A2D_EINVAL, std::to_string(H) + " query heads not divisible by " + std::to_string(H_kv) + " kv heads");
   if (Tq < 0 || Tk < 0 || Tq > INT32_MAX / 2 || Tk > INT32_MAX / 2) return fail(A2D_EINVAL, "a2d_fa_bwd_chunk: bad T");
   if (Tk == 0) return A2D_OK;
-  BwdParams p{};
-  int rc;
-  if (Tq > 0) {
-    if ((rc = make_tmap_bf16_3d(&p.tm_q, q, D, Tq, H, D, Tq * D, 64))) return rc;
-    if ((rc = make_tmap_bf16_3d(&p.tm_do, dout, D, Tq, H, D, Tq * D, 64))) return rc;
-    if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc, D, Tq, H, 128, 64))) return rc;
+  // One launch covers at most 4096 query tiles (256K rows: the kernel's
+  // shared-memory live list); longer query chunks run as consecutive slices,
+  // later slices accumulating into dk/dv.
+  constexpr int64_t kSlice = 4096 * 64;
+  const int tq_pad = (int)((Tq + 63) / 64 * 64);
+  for (int64_t off = 0; off < (Tq > 0 ? Tq : 1); off += kSlice) {
+    const int64_t len = Tq > 0 ? std::min(kSlice, Tq - off) : 0;
+    BwdParams p{};
+    int rc;
+    if ((rc = make_tmap_bf16_3d(&p.tm_k, k, D, Tk, H_kv, D, Tk * D, 128))) return rc;
+    if ((rc = make_tmap_bf16_3d(&p.tm_v, v, D, Tk, H_kv, D, Tk * D, 128))) return rc;
+    if (len > 0) {
+      const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q) + off * D;
+      const __nv_bfloat16* db = static_cast<const __nv_bfloat16*>(dout) + off * D;
+      if ((rc = make_tmap_bf16_3d(&p.tm_q, qb, D, len, H, D, Tq * D, 64))) return rc;
+      if ((rc = make_tmap_bf16_3d(&p.tm_do, db, D, len, H, D, Tq * D, 64))) return rc;
+      if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc + off * D, D, len, H, Tq * D, 128, 64))) return rc;
+    } else {
+      p.tm_q = p.tm_k;
+      p.tm_do = p.tm_k;
+      p.tm_dq = p.tm_k;
+    }
+    p.q_pos = q_pos + off;
+    p.k_pos = k_pos;
+    p.q_bounds = reinterpret_cast<const int2*>(q_bounds64) + off / 64;
+    p.k_bounds = reinterpret_cast<const int2*>(k_bounds128);
+    p.lse2 = lse2 + off;
+    p.delta = delta + off;
+    p.stats_stride = tq_pad;
+    p.dq_acc = dq_acc + off * D;
+    p.dk = dk;
+    p.dv = dv;
+    p.accumulate_kv = (accumulate_kv || off > 0) ? 1 : 0;
+    p.Tq = (int)len;
+    p.Tk = (int)Tk;
+    p.H = H;
+    p.Hkv = H_kv;
+    p.G = H / H_kv;
+    p.causal = causal;
+    p.scale = scale;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    if ((rc = cuda_status(launch_fa_bwd(p, D, S(stream)), "a2d_fa_bwd_chunk"))) return rc;
   }
-  if ((rc = make_tmap_bf16_3d(&p.tm_k, k, D, Tk, H_kv, D, Tk * D, 128))) return rc;
-  if ((rc = make_tmap_bf16_3d(&p.tm_v, v, D, Tk, H_kv, D, Tk * D, 128))) return rc;
-  if (Tq == 0) { p.tm_q = p.tm_k; p.tm_do = p.tm_k; p.tm_dq = p.tm_k; }
-  p.q_pos = q_pos;
-  p.k_pos = k_pos;
-  p.q_bounds = reinterpret_cast<const int2*>(q_bounds64);
-  p.k_bounds = reinterpret_cast<const int2*>(k_bounds128);
-  p.lse2 = lse2;
-  p.delta = delta;
-  p.dq_acc = dq_acc;
-  p.dk = dk;
-  p.dv = dv;
-  p.accumulate_kv = accumulate_kv;
-  p.Tq = (int)Tq;
-  p.Tk = (int)Tk;
-  p.H = H;
-  p.Hkv = H_kv;
-  p.G = H / H_kv;
-  p.causal = causal;
-  p.scale = scale;
-  p.scale_log2 = scale * 1.4426950408889634f;
-  return cuda_status(launch_fa_bwd(p, D, S(stream)), "a2d_fa_bwd_chunk");
+  return A2D_OK;
 }
 
 int a2d_merge(float* acc_o, float* acc_lse, const float* blk_o, const float* blk_lse, int64_t rows, int32_t D,

@@ -37,7 +37,7 @@ constexpr int BQ = 64;   // queries per iteration
 constexpr int D = 128;
 constexpr int QST = 3;   // Q/dO stages (TMA latency off the critical path)
 constexpr int kThreads = 512;
-constexpr int kMaxQTiles = 8192;                 // live-list capacity (Tq <= 512K per chunk)
+constexpr int kMaxQTiles = 4096;                 // live-list capacity per launch (the C ABI slices longer query chunks)
 constexpr uint16_t kFullBit = 0x8000;
 // smem layout (bytes, from 1 KB aligned base)
 constexpr int kK = 0;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   const int hk = blockIdx.y;
   const int key0 = kt * BK;
   const int nqt = (p.Tq + BQ - 1) / BQ;
-  const int Tq_pad = nqt * BQ;
+  const int Tq_pad = p.stats_stride;  // row stride of lse2 / delta (>= round_up(Tq, 64))
   const int2 kb = p.k_bounds[kt];
   const bool causal = p.causal != 0;
   uint16_t* live_list = reinterpret_cast<uint16_t*>(smem + kList);

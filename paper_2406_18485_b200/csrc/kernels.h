@@ -31,13 +31,14 @@ cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s);
 // D = rowsum(dO * O) of the query chunk.
 struct BwdParams {
   CUtensorMap tm_q, tm_k, tm_v, tm_do;  // box {64,64,1} for q/do, {64,128,1} for k/v
-  CUtensorMap tm_dq;                    // fp32 dq_acc [H][Tq][128], box {128,32,1}, no swizzle
+  CUtensorMap tm_dq;                    // fp32 dq_acc [H][Tq][128], box {128,64,1}, no swizzle
   const int* q_pos;
   const int* k_pos;
   const int2* q_bounds;   // per 64-row query tile
   const int2* k_bounds;   // per 128-key tile
-  const float* lse2;      // [H][Tq] LSE * log2(e)  (-inf for dead rows)
-  const float* delta;     // [H][Tq] rowsum(dO*O)
+  const float* lse2;      // [H][stats_stride] LSE * log2(e) (+inf for dead rows / padding)
+  const float* delta;     // [H][stats_stride] rowsum(dO*O)
+  int stats_stride;       // row stride of lse2 / delta
   float* dq_acc;          // [H][Tq][D] fp32, accumulated with atomics
   float* dk;              // [Hkv][Tk][D] fp32 output (or accumulated)
   float* dv;

@@ -191,3 +191,22 @@ def test_permute_and_gather_bit_exact():
     out = torch.empty((6, 3, 40, 16), dtype=torch.bfloat16, device=d)
     K.gather_blocks(x, idx, out)
     assert torch.equal(out.view(torch.int16), x.view(torch.int16)[idx.long()])
+
+
+def test_bwd_query_slicing_beyond_one_launch():
+    """Query chunks longer than one launch's live list (4096 tiles = 262144
+    rows) run as consecutive slices; dK/dV must still sum over all of them."""
+    d = dev()
+    H, Hkv, Tq, Tk, D = 2, 1, 262144 + 130, 200, 128
+    rng = np.random.Generator(np.random.Philox(91))
+    q = bf16_round(rng.standard_normal((H, Tq, D)) * 0.5)
+    k = bf16_round(rng.standard_normal((Hkv, Tk, D)) * 0.5)
+    v = bf16_round(rng.standard_normal((Hkv, Tk, D)))
+    do = bf16_round(rng.standard_normal((H, Tq, D)))
+    qpos, kpos = np.arange(Tq) + 1000, np.arange(Tk)   # every query sees every key (causal, full tiles)
+    dq, dk, dv = _bwd(q, k, v, do, qpos, kpos, True, d)
+    rows = np.concatenate([np.arange(0, 64), np.arange(262100, Tq)])
+    rq, rk, rv = orc.attention_grads(q, k, v, do, qpos, kpos, True)
+    close("dQ (sampled rows)", dq[:, rows], rq[:, rows])
+    close("dK", dk, rk)
+    close("dV", dv, rv)
