@@ -290,7 +290,10 @@ def _alltoall_move(group_vals, d_hp: int, to_head: bool):
 
 
 def _is_gpu(v) -> bool:
-    return isinstance(v, torch.Tensor) and v.is_cuda
+    """Device tensor whose per-(peer, head) blocks the 128-bit permute kernel can move."""
+    if not (isinstance(v, torch.Tensor) and v.is_cuda):
+        return False
+    return (v.shape[1] * v.shape[2] * v.element_size()) % 16 == 0
 
 
 def seq_alltoall_scatter(x: ShardedSeq, grid: RankGrid) -> ShardedSeq:
