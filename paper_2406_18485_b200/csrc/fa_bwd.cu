@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
 
   const int warp = warp_id(), lane = lane_id();
   const int nkt = (p.Tk + BK - 1) / BK;
-  const int kt = nkt - 1 - (int)blockIdx.x;  // heavy-first for causal
+  const int kt = (int)blockIdx.x;  // heavy-first: early keys are seen by the most queries (causal)
   const int hk = blockIdx.y;
   const int key0 = kt * BK;
   const int nqt = (p.Tq + BQ - 1) / BQ;
