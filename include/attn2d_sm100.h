@@ -91,6 +91,17 @@ int a2d_permute_blocks(const void* src, void* dst, int64_t A, int64_t B, int64_t
 int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, const int32_t* dst_map, int64_t n,
                       int64_t block_bytes, void* stream);
 
+/* Strided row copy: for t < n_t, h < n_h, copy row_bytes (multiple of 16)
+ * from src + t*src_st + smap(h)*src_sh to dst + t*dst_st + dmap(h)*dst_sh
+ * (all strides in BYTES; smap/dmap device int32 maps, NULL = identity).
+ * Token-major (L,H,d) <-> head-major (H,L,d) conversion fused with the
+ * SeqAlltoAll pack/unpack, including strided views of a fused QKV
+ * projection output — the data-loader side of ref shard_sequence
+ * (sharding.py:56-79). */
+int a2d_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t src_st, int64_t src_sh,
+                  int64_t dst_st, int64_t dst_sh, int64_t row_bytes, const int32_t* smap, const int32_t* dmap,
+                  void* stream);
+
 /* dst[h] = sum_r src[h*rep + r] over per_head fp32 values (gradient of kv_replicate). */
 int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream);
 

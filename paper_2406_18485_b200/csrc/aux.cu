@@ -239,3 +239,39 @@ cudaError_t launch_add_f32(float* dst, const float* src, int64_t n, int n_sm, cu
 }
 
 }  // namespace a2d
+
+namespace a2d {
+
+// dst(t, h) = src(t, smap(h)) for rows of row_vec x 16 bytes, arbitrary
+// (t, h) strides in bytes on both sides (dst head slot dmap(h) if given).
+// Token-major (L, H, d) <-> head-major (H, L, d) conversions, the fused
+// QKV-projection views and the GQA head map are all instances; the layout
+// change rides on the all-to-all pack instead of costing its own pass.
+__global__ void copy_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t n_t, int64_t n_h,
+                                 int64_t s_st, int64_t s_sh, int64_t d_st, int64_t d_sh, int64_t row_vec,
+                                 const int* __restrict__ smap, const int* __restrict__ dmap) {
+  const int64_t total = n_t * n_h * row_vec;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i % row_vec;
+    const int64_t row = i / row_vec;
+    const int64_t h = row % n_h, t = row / n_h;
+    const int64_t hs = smap ? smap[h] : h, hd = dmap ? dmap[h] : h;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + t * s_st + hs * s_sh) + e);
+    reinterpret_cast<uint4*>(dst + t * d_st + hd * d_sh)[e] = v;
+  }
+}
+
+cudaError_t launch_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t s_st, int64_t s_sh,
+                             int64_t d_st, int64_t d_sh, int64_t row_bytes, const int* smap, const int* dmap,
+                             int n_sm, cudaStream_t s) {
+  if (row_bytes % 16 != 0) return cudaErrorInvalidValue;
+  const int64_t total = n_t * n_h * (row_bytes / 16);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  copy_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n_t,
+                                                    n_h, s_st, s_sh, d_st, d_sh, row_bytes / 16, smap, dmap);
+  return cudaGetLastError();
+}
+
+}  // namespace a2d

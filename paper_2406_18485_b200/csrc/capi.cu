@@ -28,6 +28,9 @@ cudaError_t launch_sum_replicas(const float* src, float* dst, int64_t heads, int
                                 cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, int n_sm, cudaStream_t s);
 cudaError_t launch_add_f32(float* dst, const float* src, int64_t n, int n_sm, cudaStream_t s);
+cudaError_t launch_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t s_st, int64_t s_sh,
+                             int64_t d_st, int64_t d_sh, int64_t row_bytes, const int* smap, const int* dmap,
+                             int n_sm, cudaStream_t s);
 
 
 static thread_local std::string g_err;
@@ -241,6 +244,18 @@ int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, const int3
   if (n < 0 || block_bytes % 16 != 0) return fail(A2D_EINVAL, "a2d_gather_blocks: block_bytes % 16 != 0");
   return cuda_status(launch_gather_blocks(src, dst, map, dst_map, n, block_bytes, sm_count(), S(stream)),
                      "a2d_gather_blocks");
+}
+
+int a2d_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t src_st, int64_t src_sh,
+                  int64_t dst_st, int64_t dst_sh, int64_t row_bytes, const int32_t* smap, const int32_t* dmap,
+                  void* stream) {
+  if (n_t < 0 || n_h < 0 || row_bytes <= 0 || row_bytes % 16)
+    return fail(A2D_EINVAL, "a2d_copy_rows: row_bytes must be a positive multiple of 16");
+  if ((src_st | src_sh | dst_st | dst_sh) % 16 || (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(A2D_EINVAL, "a2d_copy_rows: pointers and strides must be 16-byte aligned");
+  return cuda_status(launch_copy_rows(src, dst, n_t, n_h, src_st, src_sh, dst_st, dst_sh, row_bytes, smap, dmap,
+                                      sm_count(), S(stream)),
+                     "a2d_copy_rows");
 }
 
 int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream) {

@@ -169,9 +169,22 @@ class Attn2D:
             return
         dist.all_to_all_single(out, inp, group=self.hp_group)
 
-    def _scatter_q(self, x: torch.Tensor, name: str, dk: int) -> torch.Tensor:
-        """SeqSharded (H, L, d) -> HeadSharded (Hl, C, dk) bf16."""
-        x = K.pad_dim(x, dk)
+    def _head_major_send(self, x: torch.Tensor, name: str, dk: int, token_major: bool) -> torch.Tensor:
+        """This rank's (H, L, dk) head-major bf16 send buffer for the HP all-to-all.
+
+        Token-major (L, H, d) input — possibly a strided head slice of a fused
+        QKV projection output — is converted by the pack itself (one pass)."""
+        if token_major and x.shape[-1] == dk and x.dtype == torch.bfloat16 and x.stride(-1) == 1:
+            send = self._buf(name + ".send", (x.shape[1], self.L, dk), torch.bfloat16)
+            K.copy_rows(x, send.transpose(0, 1))
+            return send
+        if token_major:
+            x = x.transpose(0, 1)
+        return K.pad_dim(x, dk)
+
+    def _scatter_q(self, x: torch.Tensor, name: str, dk: int, token_major: bool = False) -> torch.Tensor:
+        """SeqSharded (H, L, d) [or token-major (L, H, d)] -> HeadSharded (Hl, C, dk) bf16."""
+        x = self._head_major_send(x, name, dk, token_major)
         d_hp = self.par.d_hp
         if d_hp == 1:
             return x
@@ -180,13 +193,23 @@ class Attn2D:
         out = self._buf(name, (self.Hl, self.C, dk), torch.bfloat16)
         return K.permute_blocks(recv, d_hp, self.Hl, out=out)
 
-    def _scatter_kv(self, k: torch.Tensor, v: torch.Tensor, name: str, dk: int) -> torch.Tensor:
-        """SeqSharded k, v (H_kv, L, d) -> HeadSharded KV chunk (2, Hkl, C, dk) bf16."""
-        k, v = K.pad_dim(k, dk), K.pad_dim(v, dk)
+    def _scatter_kv(self, k: torch.Tensor, v: torch.Tensor, name: str, dk: int,
+                    token_major: bool = False) -> torch.Tensor:
+        """SeqSharded k, v (H_kv, L, d) [or token-major (L, H_kv, d)] -> HeadSharded
+        KV chunk (2, Hkl, C, dk) bf16. GQA replication happens in the pack's head map."""
         d_hp = self.par.d_hp
         send = self._buf(name + ".send", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16)
-        K.gather_blocks(k, self._smap, send, self._dmap_k)
-        K.gather_blocks(v, self._smap, send, self._dmap_v)
+        if token_major and k.shape[-1] == dk and k.dtype == v.dtype == torch.bfloat16 \
+                and k.stride(-1) == 1 and v.stride(-1) == 1:
+            rows = send.view(d_hp * 2 * self.Hkl, self.L, dk).transpose(0, 1)
+            K.copy_rows(k, rows, self._smap, self._dmap_k)
+            K.copy_rows(v, rows, self._smap, self._dmap_v)
+        else:
+            if token_major:
+                k, v = k.transpose(0, 1), v.transpose(0, 1)
+            k, v = K.pad_dim(k, dk), K.pad_dim(v, dk)
+            K.gather_blocks(k, self._smap, send, self._dmap_k)
+            K.gather_blocks(v, self._smap, send, self._dmap_v)
         if d_hp == 1:
             return send.view(2, self.Hkl, self.C, dk)
         recv = self._buf(name + ".recv", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16)
@@ -194,17 +217,33 @@ class Attn2D:
         out = self._buf(name, (2, self.Hkl, self.C, dk), torch.bfloat16)
         return K.permute_blocks(recv, d_hp, 2 * self.Hkl, out=out)
 
-    def _gather(self, x: torch.Tensor, name: str) -> torch.Tensor:
-        """HeadSharded (B, C, e) -> SeqSharded (d_hp*B, L, e), any dtype."""
+    def _gather(self, x: torch.Tensor, name: str, fresh: bool = False) -> torch.Tensor:
+        """HeadSharded (B, C, e) -> SeqSharded (d_hp*B, L, e), any dtype.
+        fresh=True returns newly allocated memory (results handed to the caller)."""
         d_hp = self.par.d_hp
         if d_hp == 1:
-            return x
+            return x.clone() if fresh else x
         B = x.shape[0]
         send = self._buf(name + ".send", (d_hp, B) + (self.L,) + tuple(x.shape[2:]), x.dtype)
         K.permute_blocks(x.contiguous(), B, d_hp, out=send)
-        recv = self._buf(name + ".recv", send.shape, x.dtype)
+        if fresh:
+            recv = torch.empty(send.shape, dtype=x.dtype, device=x.device)
+        else:
+            recv = self._buf(name + ".recv", send.shape, x.dtype)
         self._a2a(recv, send)
         return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
+
+    def _to_layout(self, x: torch.Tensor, token_major: bool) -> torch.Tensor:
+        """Head-major (H, L, e>=d) result -> caller's layout, head dim d, fresh memory."""
+        if not token_major:
+            return x[..., :self.d] if x.shape[-1] != self.d else x
+        out = torch.empty((x.shape[1], x.shape[0], self.d), dtype=x.dtype, device=x.device)
+        src = x[..., :self.d] if x.shape[-1] != self.d else x
+        if (self.d * x.element_size()) % 16 == 0 and src.stride(-1) == 1:
+            K.copy_rows(src.transpose(0, 1), out)
+        else:
+            out.copy_(src.transpose(0, 1))
+        return out
 
     def _p2p(self, group, send_t, to, recv_t, frm):
         if not self.comm_enabled:
@@ -306,45 +345,58 @@ class Attn2D:
         return home
 
     # ------------------------------------------------------------ public
-    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
-        """SeqSharded bf16 q (H, L, d), k/v (H_kv, L, d) -> SeqSharded out (H, L, d)."""
-        H, L, d = q.shape
-        if (H, L, d) != (self.model.heads, self.L, self.d):
-            raise ValueError(f"q must be (H={self.model.heads}, L={self.L}, d={self.d}), got {tuple(q.shape)}")
-        if tuple(k.shape) != (self.model.kv_heads, self.L, self.d) or k.shape != v.shape:
-            raise ValueError("k/v must be (H_kv, L, d)")
+    def _check_inputs(self, q, k, v, token_major):
+        H, Hkv, L, d = self.model.heads, self.model.kv_heads, self.L, self.d
+        want_q, want_kv = ((L, H, d), (L, Hkv, d)) if token_major else ((H, L, d), (Hkv, L, d))
+        if tuple(q.shape) != want_q:
+            raise ValueError(f"q must be {want_q}, got {tuple(q.shape)}")
+        if tuple(k.shape) != want_kv or tuple(v.shape) != want_kv:
+            raise ValueError(f"k/v must be {want_kv}")
+
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld") -> torch.Tensor:
+        """This rank's SeqSharded chunk -> SeqSharded output, bf16.
+
+        layout "hld": q (H, L, d), k/v (H_kv, L, d) head-major (the reference's
+        DenseTensor.values); "lhd": token-major (L, H, d) / (L, H_kv, d), strided
+        views (e.g. slices of a fused QKV projection output) accepted as is.
+        Output in the same layout."""
+        if layout not in ("hld", "lhd"):
+            raise ValueError(f"layout must be 'hld' or 'lhd', got {layout!r}")
+        tm = layout == "lhd"
+        self._check_inputs(q, k, v, tm)
         self.times.clear()
         self._mark("fwd.start")
         kd = self.kd
-        qh = self._scatter_q(q, "q", kd)
-        kvh = self._scatter_kv(k, v, "kv", kd)
+        qh = self._scatter_q(q, "q", kd, tm)
+        kvh = self._scatter_kv(k, v, "kv", kd, tm)
         self._mark("fwd.a2a_in")
-        out_h = self._buf("out_h", (self.Hl, self.C, kd), torch.bfloat16)
-        lse = self._buf("lse", (self.Hl, self.C), torch.float32)
+        out_h = torch.empty((self.Hl, self.C, kd), dtype=torch.bfloat16, device=self.device)
+        lse = torch.empty((self.Hl, self.C), dtype=torch.float32, device=self.device)
         self._ring_forward(qh, kvh, out_h, lse)
-        out = self._gather(out_h, "out")
+        out = self._gather(out_h, "out", fresh=not tm)
         self._mark("fwd.a2a_out")
         self.saved = (qh, kvh, out_h, lse)
-        return out[..., :self.d] if kd != self.d else out
+        return self._to_layout(out, tm)
 
-    def backward(self, dout: torch.Tensor):
-        """SeqSharded dout (H, L, d) -> (dq, dk, dv) SeqSharded, bf16."""
+    def backward(self, dout: torch.Tensor, layout: str = "hld"):
+        """SeqSharded dout -> (dq, dk, dv) SeqSharded, bf16, in the given layout."""
         if self.saved is None:
             raise RuntimeError("backward called before forward")
+        tm = layout == "lhd"
         qh, kvh, out_h, lse = self.saved
         self._mark("bwd.start")
         bd = self.bd
         if self.kd != bd:  # head dim <= 64: the backward kernel runs at 128 (exact zero padding)
             qh, kvh, out_h = K.pad_dim(qh, bd), K.pad_dim(kvh, bd), K.pad_dim(out_h, bd)
         out_b = out_h
-        doh = self._scatter_q(dout, "do", bd)
+        doh = self._scatter_q(dout, "do", bd, tm)
         self._mark("bwd.a2a_in")
         lse2, delta = K.bwd_preprocess(out_b, doh, lse)
         dq_acc = self._buf("dq_acc", (self.Hl, self.C, bd), torch.float32)
         dq_acc.zero_()
         dkv = self._ring_backward(qh, kvh, doh, lse2, delta, dq_acc)
         self._mark("bwd.ring")
-        dq = self._gather(K.to_bf16(dq_acc, self._buf("dq_h", dq_acc.shape, torch.bfloat16)), "dq")
+        dq = self._gather(K.to_bf16(dq_acc, self._buf("dq_h", dq_acc.shape, torch.bfloat16)), "dq", fresh=not tm)
         if self.rep == 1:
             dkv_b = K.to_bf16(dkv, self._buf("dkv_h", dkv.shape, torch.bfloat16))
             g = self._gather_kv(dkv_b, "dkv")
@@ -353,9 +405,10 @@ class Attn2D:
             g = self._gather_kv(dkv, "dkv32")
             dk = K.to_bf16(K.sum_replicas(g[0].contiguous(), self.rep))
             dv = K.to_bf16(K.sum_replicas(g[1].contiguous(), self.rep))
+        if not tm and self.rep == 1:
+            dk, dv = dk.clone(), dv.clone()  # results are handed to the caller: no aliasing of buffers
         self._mark("bwd.a2a_out")
-        sl = (lambda x: x[..., :self.d]) if bd != self.d else (lambda x: x)
-        return sl(dq), sl(dk), sl(dv)
+        return self._to_layout(dq, tm), self._to_layout(dk, tm), self._to_layout(dv, tm)
 
     def _gather_kv(self, x: torch.Tensor, name: str) -> torch.Tensor:
         """HeadSharded (2, Hkl, C, e) -> SeqSharded (2, H_rep, L, e)."""
@@ -379,14 +432,14 @@ class Attn2DFunction(torch.autograd.Function):
     """autograd wrapper: saves O and LSE (selective-checkpoint friendly), no recompute of attention."""
 
     @staticmethod
-    def forward(ctx, q, k, v, op: Attn2D):
-        ctx.op = op
-        return op.forward(q, k, v)
+    def forward(ctx, q, k, v, op: Attn2D, layout: str = "hld"):
+        ctx.op, ctx.layout = op, layout
+        return op.forward(q, k, v, layout)
 
     @staticmethod
     def backward(ctx, dout):
-        dq, dk, dv = ctx.op.backward(dout.contiguous())
-        return dq, dk, dv, None
+        dq, dk, dv = ctx.op.backward(dout, ctx.layout)
+        return dq, dk, dv, None, None
 
 
 def shard_global(x: torch.Tensor, op: Attn2D) -> torch.Tensor:

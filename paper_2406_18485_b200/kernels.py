@@ -144,6 +144,28 @@ def gather_blocks(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor,
     return out
 
 
+def copy_rows(src: torch.Tensor, dst: torch.Tensor, src_map: torch.Tensor | None = None,
+              dst_map: torch.Tensor | None = None) -> torch.Tensor:
+    """dst[t, dmap(h), :] = src[t, smap(h), :] for 3-D (T, H, row) views with any
+    (t, h) strides and a contiguous last dim — e.g. token-major <-> head-major
+    (pass ``x.transpose(0, 1)``) or a head slice of a fused QKV buffer."""
+    if src.dim() != 3 or dst.dim() != 3:
+        raise ValueError("copy_rows expects 3-D (T, H, row) views")
+    if src.stride(2) != 1 or dst.stride(2) != 1 or src.dtype != dst.dtype:
+        raise ValueError("copy_rows needs a contiguous, same-dtype last dimension")
+    n_t = src.shape[0]
+    n_h = (src_map.numel() if src_map is not None else src.shape[1])
+    es = src.element_size()
+    row = src.shape[2] * es
+    dev = src.device
+    sm = None if src_map is None else src_map.to(device=dev, dtype=torch.int32).contiguous()
+    dm = None if dst_map is None else dst_map.to(device=dev, dtype=torch.int32).contiguous()
+    _lib.call("a2d_copy_rows", src.data_ptr(), dst.data_ptr(), n_t, n_h, src.stride(0) * es, src.stride(1) * es,
+              dst.stride(0) * es, dst.stride(1) * es, row, None if sm is None else sm.data_ptr(),
+              None if dm is None else dm.data_ptr(), _stream())
+    return dst
+
+
 def sum_replicas(src: torch.Tensor, rep: int) -> torch.Tensor:
     """[H*rep, ...] fp32 -> [H, ...] summing consecutive copies."""
     heads = src.shape[0] // rep

@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 
 from oracle import attn2d_oracle as orc  # noqa: E402
 from paper_2406_18485_b200.config import ClusterConfig, ModelConfig, ParallelConfig, Placement  # noqa: E402
-from paper_2406_18485_b200.dist import Attn2D, shard_global, unshard_global  # noqa: E402
+from paper_2406_18485_b200.dist import Attn2D, Attn2DFunction, shard_global, unshard_global  # noqa: E402
 
 
 def metrics(got, ref):
@@ -44,6 +44,9 @@ def main():
     ap.add_argument("--causal", type=int, default=1)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--golden", default="")
+    ap.add_argument("--fused-qkv", action="store_true",
+                    help="token-major (L, H+2H_kv, d) fused QKV buffer, q/k/v passed as strided views, "
+                         "gradients through torch.autograd (Attn2DFunction)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
@@ -66,8 +69,19 @@ def main():
     dev = torch.device("cuda", local)
     T = lambda x: torch.from_numpy(np.asarray(x, np.float32)).to(dev).to(torch.bfloat16)  # noqa: E731
     qt, kt, vt, dot = T(q), T(k), T(v), T(do)
-    out = op.forward(shard_global(qt, op), shard_global(kt, op), shard_global(vt, op))
-    dq, dk, dv = op.backward(shard_global(dot, op))
+    if a.fused_qkv:
+        H, Hkv = a.heads, a.kv_heads
+        qkv = torch.cat([shard_global(x, op).transpose(0, 1) for x in (qt, kt, vt)], dim=1).contiguous()
+        qkv.requires_grad_(True)
+        out_tm = Attn2DFunction.apply(qkv[:, :H], qkv[:, H:H + Hkv], qkv[:, H + Hkv:], op, "lhd")
+        out_tm.backward(shard_global(dot, op).transpose(0, 1))
+        out = out_tm.detach().transpose(0, 1).contiguous()
+        g = qkv.grad
+        dq, dk, dv = (g[:, lo:hi].transpose(0, 1).contiguous()
+                      for lo, hi in ((0, H), (H, H + Hkv), (H + Hkv, H + 2 * Hkv)))
+    else:
+        out = op.forward(shard_global(qt, op), shard_global(kt, op), shard_global(vt, op))
+        dq, dk, dv = op.backward(shard_global(dot, op))
     torch.cuda.synchronize()
 
     def gather_all(x):

@@ -70,3 +70,24 @@ def test_dist_golden_config1_shape(placement, tmp_path):
         ma, rl, rng = res[name]
         assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
             f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
+
+
+FUSED = [(2, 2, 2, "head_first", 8, 2, 2048, 128), (1, 2, 1, "context_first", 4, 4, 1024, 128),
+         (4, 1, 1, "head_first", 8, 2, 1024, 128), (1, 1, 1, "head_first", 4, 2, 1024, 64)]
+
+
+@pytest.mark.parametrize("case", FUSED, ids=lambda c: "x".join(map(str, c[:3])) + f"-{c[3]}-H{c[4]}-{c[5]}-d{c[7]}")
+def test_dist_token_major_fused_qkv_autograd(case, tmp_path):
+    """Token-major strided views of a fused QKV projection output, gradients
+    through torch.autograd."""
+    d_hp, d_cp, w, pl, H, Hkv, S, d = case
+    n = d_hp * d_cp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    res = _run(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
+                   "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", str(d), "--fused-qkv"],
+               tmp_path)
+    for name in ("O", "dQ", "dK", "dV"):
+        ma, rl, rng = res[name]
+        assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
+            f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
