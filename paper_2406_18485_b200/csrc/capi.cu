@@ -210,6 +210,7 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
     p.delta = delta + off;
     p.stats_stride = tq_pad;
     p.dq_acc = dq_acc + off * D;
+    p.dq_stride_h = Tq * D;
     p.dk = dk;
     p.dv = dv;
     p.accumulate_kv = (accumulate_kv || off > 0) ? 1 : 0;

@@ -29,6 +29,10 @@
 #include "sm100.cuh"
 #include "kernels.h"
 
+#ifndef A2D_DQ_RED
+#define A2D_DQ_RED 0  // 1: dQ drained with per-element fp32 reductions instead of smem + TMA reduce
+#endif
+
 namespace a2d {
 
 namespace bwd {
@@ -285,6 +289,23 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars.dq_empty[b]);
+#if A2D_DQ_RED
+        // fp32 reductions straight from registers: for each query, the 32
+        // lanes of a warp cover 32 consecutive features (one 128 B line)
+        float* base = p.dq_acc + (size_t)h * p.dq_stride_h + (size_t)(qt * BQ) * D + d;
+        const int rows = min(BQ, p.Tq - qt * BQ);
+        if (rows == BQ) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) atomicAdd(base + (size_t)c * D, __uint_as_float(v0[c]) * scale);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) atomicAdd(base + (size_t)(c + 32) * D, __uint_as_float(v1[c]) * scale);
+        } else {
+          for (int c = 0; c < 32; ++c)
+            if (c < rows) atomicAdd(base + (size_t)c * D, __uint_as_float(v0[c]) * scale);
+          for (int c = 0; c < 32; ++c)
+            if (c + 32 < rows) atomicAdd(base + (size_t)(c + 32) * D, __uint_as_float(v1[c]) * scale);
+        }
+#else
         if (leader) bulk_wait_read0();  // previous reduce finished reading the stage
         named_bar_sync(1, 128);
 #pragma unroll
@@ -297,6 +318,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
           tma_reduce_add_3d(&p.tm_dq, dq_stage, 0, qt * BQ, h);
           bulk_commit();
         }
+#endif
       }
     }
     if (leader) bulk_wait0();

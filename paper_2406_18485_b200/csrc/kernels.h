@@ -39,7 +39,8 @@ struct BwdParams {
   const float* lse2;      // [H][stats_stride] LSE * log2(e) (+inf for dead rows / padding)
   const float* delta;     // [H][stats_stride] rowsum(dO*O)
   int stats_stride;       // row stride of lse2 / delta
-  float* dq_acc;          // [H][Tq][D] fp32, accumulated with atomics
+  float* dq_acc;          // [H][..][D] fp32 (this launch's first row), accumulated
+  int64_t dq_stride_h;    // head stride of dq_acc in elements
   float* dk;              // [Hkv][Tk][D] fp32 output (or accumulated)
   float* dv;
   int accumulate_kv;      // 1: dk/dv += partial, 0: overwrite
