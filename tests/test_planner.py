@@ -1,0 +1,64 @@
+"""B200-calibrated cost model / planner vs measured sweeps. CPU only."""
+
+import os
+
+import pytest
+
+from conftest import ROOT
+from paper_2406_18485_b200 import planner as P
+from paper_2406_18485_b200.config import ModelConfig, ParallelConfig, Placement
+
+SWEEPS = [os.path.join(ROOT, "profiles", f) for f in ("r01_sweep_S128k_2_4gpu.jsonl", "r01_sweep_S512k_2_4gpu.jsonl")]
+REF_SRC = os.environ.get("ATTN2D_REF", "/root/reference/pkg/src")
+
+
+@pytest.mark.parametrize("path", SWEEPS)
+def test_predictions_track_measured_sweeps(path):
+    r = P.check_against_sweep(path)
+    assert r["n"] == 18
+    assert r["mean_rel_err"] < 0.08 and r["max_rel_err"] < 0.15, r
+
+
+@pytest.mark.parametrize("path", SWEEPS)
+def test_planner_pick_is_near_measured_best(path):
+    import json
+    groups = {}
+    for line in open(path):
+        rec = json.loads(line)
+        s = rec["sweep"]
+        groups.setdefault((s["seq"], s["n"]), []).append((rec["ms_per_step"], s))
+    for (seq, n), rows in groups.items():
+        model = ModelConfig(seq_len=seq, heads=32, kv_heads=32, hidden=4096)
+        _, pick = P.plan(model, n)[0]
+        meas = {(s["d_hp"], s["d_cp"], s["w"], s["placement"]): t for t, s in rows}
+        t_pick = meas[(pick.d_hp, pick.d_cp, pick.inner_ring, pick.placement.value)]
+        assert t_pick <= 1.03 * min(meas.values()), (seq, n, pick, t_pick, min(meas.values()))
+
+
+def test_enumeration_counts():
+    model = ModelConfig(seq_len=524288, heads=32, kv_heads=32, hidden=4096)
+    # d_sp=2: (1,2,w1),(1,2,w2),(2,1) x 2 placements = 6; d_sp=4: 12; d_sp=8: 20
+    assert [len(P.enumerate_configs(model, n)) for n in (2, 4, 8)] == [6, 12, 20]
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not present")
+def test_enumeration_matches_reference():
+    import sys
+    sys.path.insert(0, REF_SRC)
+    import attn2d
+    for n in (2, 4, 8):
+        m = ModelConfig(seq_len=131072, heads=32, kv_heads=8, hidden=4096)
+        rm = attn2d.ModelConfig(seq_len=131072, heads=32, kv_heads=8, hidden=4096)
+        ours = {(p.d_hp, p.d_cp, p.inner_ring, p.placement.value) for p in P.enumerate_configs(m, n)}
+        ref = {(p.d_hp, p.d_cp, p.inner_ring, p.placement.value)
+               for p in attn2d.enumerate_configs(rm, n, attn2d.ClusterConfig())}
+        assert ours == ref
+
+
+def test_predict_components_sane():
+    model = ModelConfig(seq_len=131072, heads=32, kv_heads=32, hidden=4096)
+    one = P.predict(model, ParallelConfig(1, 1))
+    assert one["t_a2a"] == 0 and one["t_ring_exposed"] == 0
+    ring = P.predict(model, ParallelConfig(1, 8, inner_ring=8, placement=Placement.HEAD_FIRST))
+    assert ring["t_ring_exposed"] > 0
+    assert 800 < one["tflops_per_gpu"] < 1200
