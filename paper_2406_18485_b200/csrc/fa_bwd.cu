@@ -14,14 +14,15 @@
 // nothing). Everything is key-major so the key tile owns the 128 TMEM lanes:
 //   S^T  = K Q^T      (M=128 keys, N=64 q, K=d)   TMEM region b, cols [0,64)
 //   dP^T = V dO^T                                  TMEM region b, cols [64,128)
-//   P^T (bf16) is written back inside each warpgroup's own S^T columns
-//   (queries 0-31 -> cols [0,16), 32-63 -> cols [32,48)) and feeds dV as a
-//   TMEM operand; dQ^T = K^T dS^T (M=d, N=64 q, K=128 keys) then lands in
-//   cols [0,64)
+//   P^T and dS^T (bf16) are written back inside each warpgroup's own S^T
+//   columns (warpgroup hq: P^T -> [32hq, 32hq+16), dS^T -> [32hq+16, 32hq+32))
+//   and feed dV / dK as TMEM (TS) operands; dQ^T = K^T dS^T (M=d, N=64 q,
+//   K=128 keys) lands in the consumed dP^T columns [64,128)
 //   dV  += P^T dO     (M=128 keys, N=d, K=64 q)    TMEM [256,384)
 //   dK  += dS^T Q                                  TMEM [384,512)
-// dS^T goes through shared memory in the SW128 K-major layout; the same bytes
-// are the MN-major B operand of dQ^T, so one copy serves both GEMMs.
+// dS^T also goes through shared memory (SW128) as the MN-major B operand of
+// dQ^T; feeding dK from TMEM saves 16 KB of smem operand reads per iteration
+// (the backward is shared-memory-bandwidth bound).
 // dQ^T is drained TMEM -> smem (fp32 [q][d]) -> TMA bulk tensor reduce-add
 // into dq_acc (the add happens in L2, one 32 KB op per iteration).
 // Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 two P/dS warpgroups that split
@@ -202,7 +203,6 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       const uint64_t dQ0 = sdesc_sw128(sQ, 16, 1024), dDO0 = sdesc_sw128(sDO, 16, 1024);
       const uint64_t dKmn = sdesc_sw128(sK, 16384, 1024);  // K as MN-major A of dQ^T
       const uint64_t dDSmn = sdesc_sw128(sDS, 8192, 1024);  // dS^T as MN-major B of dQ^T
-      const uint64_t dDSk = sdesc_sw128(sDS, 16, 1024);     // dS^T as K-major A of dK
       const uint64_t dQmn = sdesc_sw128(sQ, 8192, 1024), dDOmn = sdesc_sw128(sDO, 8192, 1024);
       auto issue_s = [&](int i) {  // S^T_i and dP^T_i into region i&1, then commit s_full
         const int b = i & 1, qs = i % QST;
@@ -234,22 +234,22 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
-          // dV += P^T dO   (P^T from TMEM region b: queries 16k.. at col (k/2)*32 + (k%2)*8)
+          // dQ^T_i = K^T dS^T_i -> region b cols [64,128) (dP^T_i already consumed)
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_ss(tmem + b * 128 + 64, dKmn + (uint64_t)(k * 128), dDSmn + (uint64_t)(k * 128), id_dq, k > 0);
+          umma_commit(&bars.dq_full[b]);
+          umma_commit(&bars.ds_free);
+          // dV += P^T dO and dK += dS^T Q, both TS: the A operand comes from TMEM
+          // region b (queries 16k.. of P^T at col (k/2)*32 + (k%2)*8, dS^T at +16)
 #pragma unroll
           for (int k = 0; k < BQ / 16; ++k)
             umma_ts(tDV, tmem + b * 128 + (k / 2) * 32 + (k % 2) * 8, dDOmn + qoff + (uint64_t)(k * 128), id_kv,
                     (i > 0 || k > 0) ? 1u : 0u);
-          // dQ^T_i = K^T dS^T_i -> region b cols [0,64) (after dV read P^T: in-order)
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_ss(tmem + b * 128, dKmn + (uint64_t)(k * 128), dDSmn + (uint64_t)(k * 128), id_dq, k > 0);
-          umma_commit(&bars.dq_full[b]);
-          // dK += dS^T Q
 #pragma unroll
           for (int k = 0; k < BQ / 16; ++k)
-            umma_ss(tDK, dDSk + (uint64_t)(k * 2), dQmn + qoff + (uint64_t)(k * 128), id_kv,
+            umma_ts(tDK, tmem + b * 128 + (k / 2) * 32 + 16 + (k % 2) * 8, dQmn + qoff + (uint64_t)(k * 128), id_kv,
                     (i > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&bars.ds_free);
           umma_commit(&bars.qdo_empty[qs]);
         }
         __syncwarp();
@@ -284,8 +284,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
         tc_fence_after();
         uint32_t v0[32], v1[32];
-        tmem_ld32(tmem + lane_base + b * 128, v0);
-        tmem_ld32(tmem + lane_base + b * 128 + 32, v1);
+        tmem_ld32(tmem + lane_base + b * 128 + 64, v0);
+        tmem_ld32(tmem + lane_base + b * 128 + 96, v1);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars.dq_empty[b]);
@@ -397,9 +397,11 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
             dw[c / 2 + 1] = pack_bf16(dv[2], dv[3]);
           }
         }
-        // P^T (bf16 pairs) inside this warpgroup's own S^T columns: [c0, c0+16)
+        // P^T and dS^T (bf16 pairs) inside this warpgroup's own S^T columns:
+        // [c0, c0+16) and [c0+16, c0+32) — the TMEM A operands of dV and dK
         tmem_st16(tmem + lane_base + b * 128 + c0, pw);
-        if (it >= 1) mbar_wait(&bars.ds_free, (it - 1) & 1);  // dK/dQ^T of it-1 done reading dS
+        tmem_st16(tmem + lane_base + b * 128 + c0 + 16, dw);
+        if (it >= 1) mbar_wait(&bars.ds_free, (it - 1) & 1);  // dQ^T of it-1 done reading dS
         uint8_t* dsrow = smem + kDS;
 #pragma unroll
         for (int c8 = 0; c8 < 4; ++c8)
