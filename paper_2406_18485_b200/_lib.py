@@ -74,11 +74,13 @@ class LaunchLog:
     def __init__(self):
         self.enabled = False
         self.count = 0
+        self.by_name: dict[str, int] = {}
         self.timed: set[str] = set()
         self.events: list = []  # (name, start_event, end_event)
 
     def reset(self, timed=()):
         self.count = 0
+        self.by_name = {}
         self.timed = set(timed)
         self.events = []
 
@@ -92,6 +94,7 @@ def call(name: str, *args) -> None:
     ev = None
     if LOG.enabled:
         LOG.count += LAUNCHES.get(name, 0)
+        LOG.by_name[name] = LOG.by_name.get(name, 0) + 1
         if name in LOG.timed:
             import torch
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

@@ -135,11 +135,15 @@ int a2d_fa_fwd_chunk(const void* q, const void* k, const void* v, const int32_t*
     if ((rc = make_tmap_bf16_3d(&p.tm_q, q, D, Tq, H, D, Tq * D, 128))) return rc;
     if ((rc = make_tmap_bf16_3d(&p.tm_k, k, D, Tk, H_kv, D, Tk * D, 128))) return rc;
     if ((rc = make_tmap_bf16_3d(&p.tm_v, v, D, Tk, H_kv, D, Tk * D, 128))) return rc;
+    if ((rc = make_tmap_bf16_3d(&p.tm_k2, k, D, Tk, H_kv, D, Tk * D, 64))) return rc;
+    if ((rc = make_tmap_bf16_3d(&p.tm_v2, v, D, Tk, H_kv, D, Tk * D, 64))) return rc;
   } else {
     // no keys: still well defined (every row empty); use q for the unused maps
     if ((rc = make_tmap_bf16_3d(&p.tm_q, q, D, Tq, H, D, Tq * D, 128))) return rc;
     p.tm_k = p.tm_q;
     p.tm_v = p.tm_q;
+    p.tm_k2 = p.tm_q;
+    p.tm_v2 = p.tm_q;
   }
   p.q_pos = q_pos;
   p.k_pos = k_pos;

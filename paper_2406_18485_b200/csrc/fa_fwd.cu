@@ -63,6 +63,114 @@ __device__ __forceinline__ bool tile_live(int2 kb, int qmax, bool causal) {
   return kb.x <= kb.y && (!causal || kb.x <= qmax);
 }
 
+// Compacted list of the KV tiles (128 keys) that are live for a CTA's two
+// query tiles, with per-query-tile "needs mask" flags (kMask0/kMask1). All 12
+// warps take part; ends with __syncthreads-visible writes to `list`/`n_live`.
+__device__ __forceinline__ void build_live_list(const FwdParams& p, int2 qr0, int2 qr1, int qmax_cta, bool causal,
+                                                int nkt, uint16_t* live_list, int* warp_cnt, int* n_live) {
+  using namespace fwd;
+  const int warp = warp_id(), lane = lane_id();
+  auto classify = [&](int j, bool& lv, uint16_t& ent) {
+    const int2 kb = p.k_bounds[j];
+    lv = tile_live(kb, qmax_cta, causal);
+    const bool tail = (j + 1) * BN > p.Tk;
+    const bool m0 = tail || (causal && !(qr0.x <= qr0.y && kb.y <= qr0.x));
+    const bool m1 = tail || (causal && !(qr1.x <= qr1.y && kb.y <= qr1.x));
+    ent = (uint16_t)(j | (m0 ? kMask0 : 0) | (m1 ? kMask1 : 0));
+  };
+  const int per_warp = (nkt + 11) / 12;
+  const int lo = warp * per_warp, hi = min(nkt, lo + per_warp);
+  int cnt = 0;
+  for (int base = lo; base < hi; base += 32) {
+    const int j = base + lane;
+    bool lv = false;
+    uint16_t ent = 0;
+    if (j < hi) classify(j, lv, ent);
+    cnt += __popc(__ballot_sync(0xffffffffu, lv));
+  }
+  if (lane == 0) warp_cnt[warp] = cnt;
+  __syncthreads();
+  int off = 0;
+  for (int w = 0; w < warp; ++w) off += warp_cnt[w];
+  if (warp == 11 && lane == 0) *n_live = off + cnt;
+  for (int base = lo; base < hi; base += 32) {
+    const int j = base + lane;
+    bool lv = false;
+    uint16_t ent = 0;
+    if (j < hi) classify(j, lv, ent);
+    const unsigned m = __ballot_sync(0xffffffffu, lv);
+    if (lv) live_list[off + __popc(m & ((1u << lane) - 1u))] = ent;
+    off += __popc(m);
+  }
+}
+
+// Row epilogue shared by both forward kernels: normalise O (TMEM) by l_sum,
+// LSE, and the fused ring-step merge (ref block_update, oracle.py:111-124).
+template <int D>
+__device__ __forceinline__ void fwd_epilogue(const FwdParams& p, uint32_t tO, int h, int row, bool row_ok,
+                                             float m_used, float l_sum, bool any) {
+  const int it = any ? 1 : 0;
+  const bool alive = l_sum > 0.f;
+  const float inv = alive ? 1.f / l_sum : 0.f;
+  const float lse_blk = alive ? (m_used + __log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
+  const size_t lrow = (size_t)h * p.Tq + (row_ok ? row : 0);
+  float wa = 0.f, wb = inv, lse_new = lse_blk;
+  if (p.merge && row_ok) {
+    const float la = p.lse[lrow];
+    const float mx2 = fmaxf(la, lse_blk);
+    if (mx2 == -INFINITY) {
+      lse_new = -INFINITY;
+      wa = 0.f;
+      wb = 0.f;
+    } else {
+      const float ea = la == -INFINITY ? 0.f : __expf(la - mx2);
+      const float eb = lse_blk == -INFINITY ? 0.f : __expf(lse_blk - mx2);
+      const float z = ea + eb;
+      lse_new = mx2 + __logf(z);
+      wa = ea / z;
+      wb = eb / z * inv;
+    }
+  }
+  if (row_ok) p.lse[lrow] = lse_new;
+  float* acc = (p.acc_o && row_ok) ? p.acc_o + ((size_t)h * p.Tq + row) * D : nullptr;
+  __nv_bfloat16* out =
+      (p.out && row_ok) ? p.out + (size_t)h * p.out_stride_h + (size_t)row * p.out_stride_t : nullptr;
+#pragma unroll 1
+  for (int c = 0; c < D / 32; ++c) {
+    uint32_t r[32];
+    if (it > 0) {
+      tmem_ld32(tO + c * 32, r);
+      tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = 0u;
+    }
+    if (!row_ok) continue;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[i + e]) * wb;
+      if (p.merge) {
+        const float4 a0 = *reinterpret_cast<const float4*>(acc + c * 32 + i);
+        const float4 a1 = *reinterpret_cast<const float4*>(acc + c * 32 + i + 4);
+        v[0] += a0.x * wa; v[1] += a0.y * wa; v[2] += a0.z * wa; v[3] += a0.w * wa;
+        v[4] += a1.x * wa; v[5] += a1.y * wa; v[6] += a1.z * wa; v[7] += a1.w * wa;
+      }
+      if (acc) {
+        *reinterpret_cast<float4*>(acc + c * 32 + i) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(acc + c * 32 + i + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      }
+      if (out) {
+        uint4 u;
+        u.x = pack_bf16(v[0], v[1]); u.y = pack_bf16(v[2], v[3]);
+        u.z = pack_bf16(v[4], v[5]); u.w = pack_bf16(v[6], v[7]);
+        *reinterpret_cast<uint4*>(out + c * 32 + i) = u;
+      }
+    }
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_constant__ FwdParams p) {
   using namespace fwd;
@@ -106,40 +214,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   // ---- compacted list of live KV tiles for this CTA (causal-dead tiles
   // never cost a loop iteration), with per-query-tile "needs mask" flags.
   uint16_t* live_list = reinterpret_cast<uint16_t*>(smem + L::kList);
-  {
-    auto classify = [&](int j, bool& lv, uint16_t& ent) {
-      const int2 kb = p.k_bounds[j];
-      lv = tile_live(kb, qmax_cta, causal);
-      const bool tail = (j + 1) * BN > p.Tk;
-      const bool m0 = tail || (causal && !(qr0.x <= qr0.y && kb.y <= qr0.x));
-      const bool m1 = tail || (causal && !(qr1.x <= qr1.y && kb.y <= qr1.x));
-      ent = (uint16_t)(j | (m0 ? kMask0 : 0) | (m1 ? kMask1 : 0));
-    };
-    const int per_warp = (nkt + 11) / 12;
-    const int lo = warp * per_warp, hi = min(nkt, lo + per_warp);
-    int cnt = 0;
-    for (int base = lo; base < hi; base += 32) {
-      const int j = base + lane;
-      bool lv = false;
-      uint16_t ent = 0;
-      if (j < hi) classify(j, lv, ent);
-      cnt += __popc(__ballot_sync(0xffffffffu, lv));
-    }
-    if (lane == 0) bars.warp_cnt[warp] = cnt;
-    __syncthreads();
-    int off = 0;
-    for (int w = 0; w < warp; ++w) off += bars.warp_cnt[w];
-    if (warp == 11 && lane == 0) bars.n_live = off + cnt;
-    for (int base = lo; base < hi; base += 32) {
-      const int j = base + lane;
-      bool lv = false;
-      uint16_t ent = 0;
-      if (j < hi) classify(j, lv, ent);
-      const unsigned m = __ballot_sync(0xffffffffu, lv);
-      if (lv) live_list[off + __popc(m & ((1u << lane) - 1u))] = ent;
-      off += __popc(m);
-    }
-  }
+  build_live_list(p, qr0, qr1, qmax_cta, causal, nkt, live_list, bars.warp_cnt, &bars.n_live);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -362,65 +437,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       mbar_wait(&bars.o_full[t], 0);
       tc_fence_after();
     }
-    const bool alive = l_sum > 0.f;
-    const float inv = alive ? 1.f / l_sum : 0.f;
-    const float lse_blk = alive ? (m_used + __log2f(l_sum)) * 0.69314718055994531f : -INFINITY;
-    const size_t lrow = (size_t)h * p.Tq + (row_ok ? row : 0);
-    float wa = 0.f, wb = inv, lse_new = lse_blk;
-    if (p.merge && row_ok) {
-      const float la = p.lse[lrow];
-      const float mx2 = fmaxf(la, lse_blk);
-      if (mx2 == -INFINITY) {
-        lse_new = -INFINITY;
-        wa = 0.f;
-        wb = 0.f;
-      } else {
-        const float ea = la == -INFINITY ? 0.f : __expf(la - mx2);
-        const float eb = lse_blk == -INFINITY ? 0.f : __expf(lse_blk - mx2);
-        const float z = ea + eb;
-        lse_new = mx2 + __logf(z);
-        wa = ea / z;
-        wb = eb / z * inv;
-      }
-    }
-    if (row_ok) p.lse[lrow] = lse_new;
-    float* acc = (p.acc_o && row_ok) ? p.acc_o + ((size_t)h * p.Tq + row) * D : nullptr;
-    __nv_bfloat16* out =
-        (p.out && row_ok) ? p.out + (size_t)h * p.out_stride_h + (size_t)row * p.out_stride_t : nullptr;
-#pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      if (it > 0) {
-        tmem_ld32(tO + c * 32, r);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = 0u;
-      }
-      if (!row_ok) continue;
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[i + e]) * wb;
-        if (p.merge) {
-          const float4 a0 = *reinterpret_cast<const float4*>(acc + c * 32 + i);
-          const float4 a1 = *reinterpret_cast<const float4*>(acc + c * 32 + i + 4);
-          v[0] += a0.x * wa; v[1] += a0.y * wa; v[2] += a0.z * wa; v[3] += a0.w * wa;
-          v[4] += a1.x * wa; v[5] += a1.y * wa; v[6] += a1.z * wa; v[7] += a1.w * wa;
-        }
-        if (acc) {
-          *reinterpret_cast<float4*>(acc + c * 32 + i) = make_float4(v[0], v[1], v[2], v[3]);
-          *reinterpret_cast<float4*>(acc + c * 32 + i + 4) = make_float4(v[4], v[5], v[6], v[7]);
-        }
-        if (out) {
-          uint4 u;
-          u.x = pack_bf16(v[0], v[1]); u.y = pack_bf16(v[2], v[3]);
-          u.z = pack_bf16(v[4], v[5]); u.w = pack_bf16(v[6], v[7]);
-          *reinterpret_cast<uint4*>(out + c * 32 + i) = u;
-        }
-      }
-    }
+    fwd_epilogue<D>(p, tO, h, row, row_ok, m_used, l_sum, it > 0);
   }
 
   tc_fence_before();

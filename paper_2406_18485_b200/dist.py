@@ -169,36 +169,43 @@ class Attn2D:
             return
         dist.all_to_all_single(out, inp, group=self.hp_group)
 
-    def _head_major_send(self, x: torch.Tensor, name: str, dk: int, token_major: bool) -> torch.Tensor:
+    def _new(self, name: str, shape, dtype, fresh: bool) -> torch.Tensor:
+        """Workspace buffer, or newly allocated memory when the result outlives the call."""
+        return torch.empty(shape, dtype=dtype, device=self.device) if fresh else self._buf(name, shape, dtype)
+
+    def _head_major_send(self, x: torch.Tensor, name: str, dk: int, token_major: bool,
+                         fresh: bool = False) -> torch.Tensor:
         """This rank's (H, L, dk) head-major bf16 send buffer for the HP all-to-all.
 
         Token-major (L, H, d) input — possibly a strided head slice of a fused
         QKV projection output — is converted by the pack itself (one pass)."""
         if token_major and x.shape[-1] == dk and x.dtype == torch.bfloat16 and x.stride(-1) == 1:
-            send = self._buf(name + ".send", (x.shape[1], self.L, dk), torch.bfloat16)
+            send = self._new(name + ".send", (x.shape[1], self.L, dk), torch.bfloat16, fresh)
             K.copy_rows(x, send.transpose(0, 1))
             return send
         if token_major:
             x = x.transpose(0, 1)
         return K.pad_dim(x, dk)
 
-    def _scatter_q(self, x: torch.Tensor, name: str, dk: int, token_major: bool = False) -> torch.Tensor:
-        """SeqSharded (H, L, d) [or token-major (L, H, d)] -> HeadSharded (Hl, C, dk) bf16."""
-        x = self._head_major_send(x, name, dk, token_major)
+    def _scatter_q(self, x: torch.Tensor, name: str, dk: int, token_major: bool = False,
+                   fresh: bool = False) -> torch.Tensor:
+        """SeqSharded (H, L, d) [or token-major (L, H, d)] -> HeadSharded (Hl, C, dk) bf16.
+        fresh=True: the result owns its memory (it is kept for the backward)."""
         d_hp = self.par.d_hp
+        x = self._head_major_send(x, name, dk, token_major, fresh and d_hp == 1)
         if d_hp == 1:
             return x
         recv = self._buf(name + ".recv", (d_hp, self.Hl, self.L, dk), torch.bfloat16)
         self._a2a(recv, x)
-        out = self._buf(name, (self.Hl, self.C, dk), torch.bfloat16)
+        out = self._new(name, (self.Hl, self.C, dk), torch.bfloat16, fresh)
         return K.permute_blocks(recv, d_hp, self.Hl, out=out)
 
     def _scatter_kv(self, k: torch.Tensor, v: torch.Tensor, name: str, dk: int,
-                    token_major: bool = False) -> torch.Tensor:
+                    token_major: bool = False, fresh: bool = False) -> torch.Tensor:
         """SeqSharded k, v (H_kv, L, d) [or token-major (L, H_kv, d)] -> HeadSharded
         KV chunk (2, Hkl, C, dk) bf16. GQA replication happens in the pack's head map."""
         d_hp = self.par.d_hp
-        send = self._buf(name + ".send", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16)
+        send = self._new(name + ".send", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16, fresh and d_hp == 1)
         if token_major and k.shape[-1] == dk and k.dtype == v.dtype == torch.bfloat16 \
                 and k.stride(-1) == 1 and v.stride(-1) == 1:
             rows = send.view(d_hp * 2 * self.Hkl, self.L, dk).transpose(0, 1)
@@ -214,7 +221,7 @@ class Attn2D:
             return send.view(2, self.Hkl, self.C, dk)
         recv = self._buf(name + ".recv", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16)
         self._a2a(recv, send)
-        out = self._buf(name, (2, self.Hkl, self.C, dk), torch.bfloat16)
+        out = self._new(name, (2, self.Hkl, self.C, dk), torch.bfloat16, fresh)
         return K.permute_blocks(recv, d_hp, 2 * self.Hkl, out=out)
 
     def _gather(self, x: torch.Tensor, name: str, fresh: bool = False) -> torch.Tensor:
@@ -353,37 +360,63 @@ class Attn2D:
         if tuple(k.shape) != want_kv or tuple(v.shape) != want_kv:
             raise ValueError(f"k/v must be {want_kv}")
 
-    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld") -> torch.Tensor:
-        """This rank's SeqSharded chunk -> SeqSharded output, bf16.
-
-        layout "hld": q (H, L, d), k/v (H_kv, L, d) head-major (the reference's
-        DenseTensor.values); "lhd": token-major (L, H, d) / (L, H_kv, d), strided
-        views (e.g. slices of a fused QKV projection output) accepted as is.
-        Output in the same layout."""
+    @staticmethod
+    def _layout(layout: str) -> bool:
         if layout not in ("hld", "lhd"):
             raise ValueError(f"layout must be 'hld' or 'lhd', got {layout!r}")
-        tm = layout == "lhd"
+        return layout == "lhd"
+
+    def scatter_inputs(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld"):
+        """SeqSharded q, k, v -> HeadSharded (qh, kvh) in memory they own (ref
+        seq_alltoall_scatter + kv_replicate, sharding.py:109-152)."""
+        tm = self._layout(layout)
+        self._check_inputs(q, k, v, tm)
+        kd = self.kd
+        return self._scatter_q(q, "q", kd, tm, fresh=True), self._scatter_kv(k, v, "kv", kd, tm, fresh=True)
+
+    def gather_output(self, out_h: torch.Tensor, layout: str = "hld") -> torch.Tensor:
+        """HeadSharded O -> SeqSharded O in the caller's layout (ref seq_alltoall_gather)."""
+        tm = self._layout(layout)
+        return self._to_layout(self._gather(out_h, "out", fresh=not tm), tm)
+
+    def forward_with_state(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld"):
+        """forward() returning (out, state); state = (qh, kvh, out_h, lse) owns its
+        memory, so any number of calls (layers) can be in flight before their backward."""
+        tm = self._layout(layout)
         self._check_inputs(q, k, v, tm)
         self.times.clear()
         self._mark("fwd.start")
         kd = self.kd
-        qh = self._scatter_q(q, "q", kd, tm)
-        kvh = self._scatter_kv(k, v, "kv", kd, tm)
+        qh = self._scatter_q(q, "q", kd, tm, fresh=True)
+        kvh = self._scatter_kv(k, v, "kv", kd, tm, fresh=True)
         self._mark("fwd.a2a_in")
         out_h = torch.empty((self.Hl, self.C, kd), dtype=torch.bfloat16, device=self.device)
         lse = torch.empty((self.Hl, self.C), dtype=torch.float32, device=self.device)
         self._ring_forward(qh, kvh, out_h, lse)
         out = self._gather(out_h, "out", fresh=not tm)
         self._mark("fwd.a2a_out")
-        self.saved = (qh, kvh, out_h, lse)
-        return self._to_layout(out, tm)
+        return self._to_layout(out, tm), (qh, kvh, out_h, lse)
 
-    def backward(self, dout: torch.Tensor, layout: str = "hld"):
-        """SeqSharded dout -> (dq, dk, dv) SeqSharded, bf16, in the given layout."""
-        if self.saved is None:
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld") -> torch.Tensor:
+        """This rank's SeqSharded chunk -> SeqSharded output, bf16.
+
+        layout "hld": q (H, L, d), k/v (H_kv, L, d) head-major (the reference's
+        DenseTensor.values); "lhd": token-major (L, H, d) / (L, H_kv, d), strided
+        views (e.g. slices of a fused QKV projection output) accepted as is.
+        Output in the same layout. The state for backward() is kept on the op
+        (last call); autograd use goes through Attn2DFunction, which keeps one
+        state per call."""
+        out, self.saved = self.forward_with_state(q, k, v, layout)
+        return out
+
+    def backward(self, dout: torch.Tensor, layout: str = "hld", state=None):
+        """SeqSharded dout -> (dq, dk, dv) SeqSharded, bf16, in the given layout.
+        `state` is a forward_with_state() state (default: the last forward())."""
+        tm = self._layout(layout)
+        state = state if state is not None else self.saved
+        if state is None:
             raise RuntimeError("backward called before forward")
-        tm = layout == "lhd"
-        qh, kvh, out_h, lse = self.saved
+        qh, kvh, out_h, lse = state
         self._mark("bwd.start")
         bd = self.bd
         if self.kd != bd:  # head dim <= 64: the backward kernel runs at 128 (exact zero padding)
@@ -434,11 +467,13 @@ class Attn2DFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, op: Attn2D, layout: str = "hld"):
         ctx.op, ctx.layout = op, layout
-        return op.forward(q, k, v, layout)
+        out, ctx.state = op.forward_with_state(q, k, v, layout)
+        return out
 
     @staticmethod
     def backward(ctx, dout):
-        dq, dk, dv = ctx.op.backward(dout, ctx.layout)
+        dq, dk, dv = ctx.op.backward(dout.contiguous() if ctx.layout == "hld" else dout, ctx.layout, ctx.state)
+        ctx.state = None
         return dq, dk, dv, None, None
 
 

@@ -91,3 +91,30 @@ def test_dist_token_major_fused_qkv_autograd(case, tmp_path):
         ma, rl, rng = res[name]
         assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
             f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
+
+
+SCPP = [(1, 1, 1), (2, 1, 1), (1, 2, 2), (2, 2, 1)]
+
+
+@pytest.mark.parametrize("case", SCPP, ids=lambda c: "x".join(map(str, c)))
+def test_selective_checkpoint_pp(case, tmp_path):
+    """SC++ (SURVEY §8f row 2): checkpointed layers recompute everything except
+    the whitelisted 2D attention, whose O/LSE are kept — same gradients as plain
+    autograd, no attention-forward kernel in the backward pass, while
+    torch.utils.checkpoint re-runs the ring forward."""
+    d_hp, d_cp, w = case
+    n = d_hp * d_cp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "tests", "scpp_check.py"),
+           "--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for res in json.loads(out.read_text()):
+        assert res["grad_rel_l2"] <= 1e-2, res
+        assert res["out_max_abs"] == 0.0, res
+        k = res["fwd_kernels_in_bwd"]
+        assert k["plain"] == 0 and k["scpp"] == 0, res
+        assert k["torch_checkpoint"] >= 2 * d_cp, res  # 2 layers x d_cp ring steps recomputed
