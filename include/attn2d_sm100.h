@@ -105,6 +105,12 @@ int a2d_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t 
 /* dst[h] = sum_r src[h*rep + r] over per_head fp32 values (gradient of kv_replicate). */
 int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream);
 
+/* dst[b][a][:] = bf16(src[a][b][:]) for fp32 blocks of block_elems (multiple
+ * of 8): the fp32 -> bf16 conversion of dQ / dK / dV fused with the pack of the
+ * gradient all-to-all (ref seq_alltoall_gather, sharding.py:155-169). A = 1
+ * or B = 1 is a plain conversion. */
+int a2d_permute_f32_to_bf16(const float* src, void* dst, int64_t A, int64_t B, int64_t block_elems, void* stream);
+
 /* Elementwise helpers (n multiple of 4). */
 int a2d_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 int a2d_add_f32(float* dst, const float* src, int64_t n, void* stream);

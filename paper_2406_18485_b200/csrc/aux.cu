@@ -152,6 +152,38 @@ cudaError_t launch_permute_blocks(const void* src, void* dst, int64_t A, int64_t
   return cudaGetLastError();
 }
 
+// dst[b][a][:] = bf16(src[a][b][:]) over blocks of blk8*8 fp32 values: the
+// fp32 -> bf16 conversion fused into the all-to-all pack of the gradient
+// gather (one HBM pass instead of convert + permute).
+__global__ void permute_f32_bf16_kernel(const float4* __restrict__ src, uint4* __restrict__ dst, int64_t A, int64_t B,
+                                        int64_t blk8) {
+  const int64_t total = A * B * blk8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i % blk8;
+    const int64_t ab = i / blk8;
+    const int64_t b = ab / A, a = ab % A;
+    const float4* s2 = src + ((a * B + b) * blk8 + e) * 2;
+    const float4 x = __ldg(s2), y = __ldg(s2 + 1);
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(x.x, x.y), p1 = __floats2bfloat162_rn(x.z, x.w);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(y.x, y.y), p3 = __floats2bfloat162_rn(y.z, y.w);
+    dst[i] = make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                        *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+  }
+}
+
+cudaError_t launch_permute_f32_bf16(const float* src, __nv_bfloat16* dst, int64_t A, int64_t B, int64_t blk_elems,
+                                    int n_sm, cudaStream_t s) {
+  if (blk_elems % 8 != 0) return cudaErrorInvalidValue;
+  const int64_t total = A * B * (blk_elems / 8);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = (int64_t)n_sm * 8;
+  if (blocks > cap) blocks = cap;
+  permute_f32_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(src),
+                                                           reinterpret_cast<uint4*>(dst), A, B, blk_elems / 8);
+  return cudaGetLastError();
+}
+
 __global__ void gather_blocks_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                      const int* __restrict__ map, const int* __restrict__ dmap, int64_t n,
                                      int64_t blk_vec) {

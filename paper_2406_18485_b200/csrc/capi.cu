@@ -27,6 +27,8 @@ cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, con
 cudaError_t launch_sum_replicas(const float* src, float* dst, int64_t heads, int rep, int64_t per_head, int n_sm,
                                 cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, int n_sm, cudaStream_t s);
+cudaError_t launch_permute_f32_bf16(const float* src, __nv_bfloat16* dst, int64_t A, int64_t B, int64_t blk_elems,
+                                    int n_sm, cudaStream_t s);
 cudaError_t launch_add_f32(float* dst, const float* src, int64_t n, int n_sm, cudaStream_t s);
 cudaError_t launch_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t s_st, int64_t s_sh,
                              int64_t d_st, int64_t d_sh, int64_t row_bytes, const int* smap, const int* dmap,
@@ -135,15 +137,11 @@ int a2d_fa_fwd_chunk(const void* q, const void* k, const void* v, const int32_t*
     if ((rc = make_tmap_bf16_3d(&p.tm_q, q, D, Tq, H, D, Tq * D, 128))) return rc;
     if ((rc = make_tmap_bf16_3d(&p.tm_k, k, D, Tk, H_kv, D, Tk * D, 128))) return rc;
     if ((rc = make_tmap_bf16_3d(&p.tm_v, v, D, Tk, H_kv, D, Tk * D, 128))) return rc;
-    if ((rc = make_tmap_bf16_3d(&p.tm_k2, k, D, Tk, H_kv, D, Tk * D, 64))) return rc;
-    if ((rc = make_tmap_bf16_3d(&p.tm_v2, v, D, Tk, H_kv, D, Tk * D, 64))) return rc;
   } else {
     // no keys: still well defined (every row empty); use q for the unused maps
     if ((rc = make_tmap_bf16_3d(&p.tm_q, q, D, Tq, H, D, Tq * D, 128))) return rc;
     p.tm_k = p.tm_q;
     p.tm_v = p.tm_q;
-    p.tm_k2 = p.tm_q;
-    p.tm_v2 = p.tm_q;
   }
   p.q_pos = q_pos;
   p.k_pos = k_pos;
@@ -273,6 +271,16 @@ int a2d_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
   if (n < 0 || n % 4) return fail(A2D_EINVAL, "a2d_f32_to_bf16: n must be a multiple of 4");
   return cuda_status(launch_f32_to_bf16(src, static_cast<__nv_bfloat16*>(dst), n, sm_count(), S(stream)),
                      "a2d_f32_to_bf16");
+}
+
+int a2d_permute_f32_to_bf16(const float* src, void* dst, int64_t A, int64_t B, int64_t block_elems, void* stream) {
+  if (A < 0 || B < 0 || block_elems % 8 != 0)
+    return fail(A2D_EINVAL, "a2d_permute_f32_to_bf16: block_elems must be a multiple of 8");
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(A2D_EINVAL, "a2d_permute_f32_to_bf16: pointers must be 16-byte aligned");
+  return cuda_status(launch_permute_f32_bf16(src, static_cast<__nv_bfloat16*>(dst), A, B, block_elems, sm_count(),
+                                             S(stream)),
+                     "a2d_permute_f32_to_bf16");
 }
 
 int a2d_add_f32(float* dst, const float* src, int64_t n, void* stream) {

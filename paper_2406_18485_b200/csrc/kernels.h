@@ -11,7 +11,6 @@ namespace a2d {
 // Forward chunk attention (one ring step). Tensors are head-major [H][T][D].
 struct FwdParams {
   CUtensorMap tm_q, tm_k, tm_v;  // bf16 [H|Hkv][T][D], box {64,128,1}, SW128
-  CUtensorMap tm_k2, tm_v2;      // K / V with box {64,64,1}: 64-key steps
   const int* q_pos;              // [Tq] original token positions
   const int* k_pos;              // [Tk]
   const int2* q_bounds;          // [ceil(Tq/128)] (min,max) position per query tile

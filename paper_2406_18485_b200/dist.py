@@ -240,6 +240,19 @@ class Attn2D:
         self._a2a(recv, send)
         return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
 
+    def _gather_f32(self, x: torch.Tensor, name: str, fresh: bool = False) -> torch.Tensor:
+        """HeadSharded fp32 (B, C, e) -> SeqSharded bf16 (d_hp*B, L, e): the
+        fp32 -> bf16 rounding is fused into the all-to-all pack (one pass)."""
+        d_hp = self.par.d_hp
+        B = x.shape[0]
+        if d_hp == 1:
+            return K.permute_to_bf16(x, 1, 1, out=self._new(name + ".bf16", x.shape, torch.bfloat16, fresh))
+        send = self._buf(name + ".send", (d_hp, B, self.L) + tuple(x.shape[2:]), torch.bfloat16)
+        K.permute_to_bf16(x, B, d_hp, out=send)
+        recv = self._new(name + ".recv", send.shape, torch.bfloat16, fresh)
+        self._a2a(recv, send)
+        return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
+
     def _to_layout(self, x: torch.Tensor, token_major: bool) -> torch.Tensor:
         """Head-major (H, L, e>=d) result -> caller's layout, head dim d, fresh memory."""
         if not token_major:
@@ -271,6 +284,7 @@ class Attn2D:
         if d_cp == 1:
             K.fwd_chunk(qh, kv_own[0], kv_own[1], qplan, self.plans[self.cp], self.causal, self.scale,
                         lse, None, out_h)
+            self._mark("fwd.step0")
             return
         acc = self._buf("fwd.acc", (self.Hl, self.C, kd), torch.float32)
         inner = [self._buf(f"kv.in{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
@@ -308,6 +322,7 @@ class Attn2D:
             dkv = self._buf("bwd.dkv_home", shape, torch.float32)
             K.bwd_chunk(qh, kv_own[0], kv_own[1], doh, qplan, self.plans[self.cp], lse2, delta, dq_acc,
                         dkv[0], dkv[1], False, self.causal, self.scale)
+            self._mark("bwd.step0")
             return dkv
         part = self._buf("bwd.part", shape, torch.float32)
         acc = [self._buf(f"bwd.acc{i}", shape, torch.float32) for i in range(2)]
@@ -429,31 +444,16 @@ class Attn2D:
         dq_acc.zero_()
         dkv = self._ring_backward(qh, kvh, doh, lse2, delta, dq_acc)
         self._mark("bwd.ring")
-        dq = self._gather(K.to_bf16(dq_acc, self._buf("dq_h", dq_acc.shape, torch.bfloat16)), "dq", fresh=not tm)
+        dq = self._gather_f32(dq_acc, "dq", fresh=not tm)
+        self._mark("bwd.a2a_dq")
         if self.rep == 1:
-            dkv_b = K.to_bf16(dkv, self._buf("dkv_h", dkv.shape, torch.bfloat16))
-            g = self._gather_kv(dkv_b, "dkv")
-            dk, dv = g[0], g[1]
-        else:
-            g = self._gather_kv(dkv, "dkv32")
-            dk = K.to_bf16(K.sum_replicas(g[0].contiguous(), self.rep))
-            dv = K.to_bf16(K.sum_replicas(g[1].contiguous(), self.rep))
-        if not tm and self.rep == 1:
-            dk, dv = dk.clone(), dv.clone()  # results are handed to the caller: no aliasing of buffers
+            # one all-to-all per tensor: each receive buffer is already (H_kv, L, e)
+            dk, dv = self._gather_f32(dkv[0], "dk", fresh=not tm), self._gather_f32(dkv[1], "dv", fresh=not tm)
+        else:  # GQA replicas: gather fp32, sum the Ĥ/H_kv copies, then round once
+            dk = K.to_bf16(K.sum_replicas(self._gather(dkv[0], "dk32"), self.rep))
+            dv = K.to_bf16(K.sum_replicas(self._gather(dkv[1], "dv32"), self.rep))
         self._mark("bwd.a2a_out")
         return self._to_layout(dq, tm), self._to_layout(dk, tm), self._to_layout(dv, tm)
-
-    def _gather_kv(self, x: torch.Tensor, name: str) -> torch.Tensor:
-        """HeadSharded (2, Hkl, C, e) -> SeqSharded (2, H_rep, L, e)."""
-        d_hp = self.par.d_hp
-        if d_hp == 1:
-            return x
-        e = x.shape[-1]
-        flat = x.reshape(2 * self.Hkl, self.C, e)
-        g = self._gather(flat, name)                       # [peer][2][Hkl][L][e]
-        out = self._buf(name + ".kv", (2, d_hp, self.Hkl, self.L, e), x.dtype)
-        K.permute_blocks(g.view(d_hp, 2, self.Hkl, self.L, e), d_hp, 2, out=out)
-        return out.view(2, self.H_rep, self.L, e)
 
     def flops(self) -> float:
         """Algorithmic fwd+bwd FLOPs of the whole layer (all ranks): 3.5 x 4 S^2 H d x (1/2 if causal)."""

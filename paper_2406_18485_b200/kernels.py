@@ -181,6 +181,16 @@ def to_bf16(src: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     return out
 
 
+def permute_to_bf16(src: torch.Tensor, A: int, B: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[b][a] = bf16(src[a][b]) with fp32 src viewed as [A][B][blk] (convert fused into the pack)."""
+    src = src.contiguous()
+    if out is None:
+        out = torch.empty(src.shape, dtype=BF16, device=src.device)
+    blk = src.numel() // max(A * B, 1)
+    _lib.call("a2d_permute_f32_to_bf16", src.data_ptr(), out.data_ptr(), A, B, blk, _stream())
+    return out
+
+
 def add_(dst: torch.Tensor, src: torch.Tensor) -> None:
     _lib.call("a2d_add_f32", dst.data_ptr(), src.data_ptr(), dst.numel(), _stream())
 

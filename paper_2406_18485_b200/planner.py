@@ -26,14 +26,18 @@ from .config import ClusterConfig, ModelConfig, ParallelConfig, Placement, repli
 
 @dataclass(frozen=True)
 class B200Calibration:
-    """Measured on B200 (round 1): tools/kbench.py, bench.py sweeps, guide peaks."""
+    """Measured on B200 (round 1): tools/kbench.py, bench.py sweeps, tools/trace.py
+    phase traces (profiles/r01_trace_*.json), guide peaks."""
 
     fwd_tflops: float = 1100.0     # forward chunk kernel in a full step (kbench alone: 1152 at S=128K)
     bwd_tflops: float = 940.0      # backward chunk kernel in a full step (kbench alone: 980)
     short_chunk_tokens: float = 500.0   # kernel efficiency ~ C / (C + this) for small chunks
-    a2a_gbs: float = 600.0         # per-GPU all-to-all bandwidth over NVLink 5 (bytes leaving a GPU)
+    a2a_gbs: float = 620.0         # NCCL all_to_all_single: time ~ whole buffer / this (traces, d_hp = 2 and 4)
     p2p_gbs: float = 770.0         # per-direction peer bandwidth (B200 profiling guide)
-    hbm_gbs: float = 6527.5        # MEASURED_PEAKS hbm_gbs (pack/unpack, K4 add)
+    hbm_gbs: float = 6527.5        # MEASURED_PEAKS hbm_gbs (K4 add)
+    pack_gbs: float = 5500.0       # achieved by the pack / permute / convert kernels (traces)
+    ring_overhead: float = 0.045   # d_cp > 1: ring-step compute slowdown (per-step merge / K4 traffic,
+                                   # smaller chunks, NCCL copy kernels sharing SMs) — sweeps and traces
     launch_s: float = 12e-6        # per NCCL call / kernel launch overhead
     elem: int = 2                  # bf16
 
@@ -58,14 +62,24 @@ def predict(model: ModelConfig, par: ParallelConfig, cal: B200Calibration | None
     frac = 0.5 if causal else 1.0
     flops = 4.0 * S * S * H * d * frac / d_sp           # forward FLOPs per GPU
     eff = _eff(cal, C)
-    t_fwd = flops / (cal.fwd_tflops * 1e12 * eff)
-    t_bwd = 2.5 * flops / (cal.bwd_tflops * 1e12 * eff)
-    # head-parallel all-to-all (critical path): fwd q,k,v in + o out; bwd do in + dq,dk,dv out
-    out_frac = (d_hp - 1) / d_hp
-    tok_bytes = L * d * cal.elem
-    a2a_fwd = (H + 2 * Hrep + H) * tok_bytes * out_frac
-    a2a_bwd = (H + H + 2 * Hrep) * tok_bytes * out_frac
-    t_a2a = (a2a_fwd + a2a_bwd) / (cal.a2a_gbs * 1e9) + (8 * cal.launch_s if d_hp > 1 else 0.0)
+    ring = 1.0 + (cal.ring_overhead if d_cp > 1 else 0.0)
+    t_fwd = ring * flops / (cal.fwd_tflops * 1e12 * eff)
+    t_bwd = ring * 2.5 * flops / (cal.bwd_tflops * 1e12 * eff)
+    # head-parallel exchange phases (critical path), as implemented in dist.Attn2D:
+    # fwd in q,k,v / out O, bwd in dO / out dQ,dK,dV (fp32 -> bf16 fused into the pack)
+    Tq = H * L * d * cal.elem               # bytes of one (H, L, d) bf16 tensor per rank
+    Tkv = 2 * Hrep * L * d * cal.elem       # k and v after replication
+    hbm = lambda b: b / (cal.pack_gbs * 1e9)  # noqa: E731
+    if d_hp > 1:
+        net = lambda b: b / (cal.a2a_gbs * 1e9) + cal.launch_s  # noqa: E731
+        t_fwd_in = net(Tq) + net(Tkv) + hbm(2 * Tkv + 2 * (Tq + Tkv))   # kv pack, unpack permutes
+        t_fwd_out = net(Tq) + hbm(2 * Tq)
+        t_bwd_in = net(Tq) + hbm(2 * Tq)
+        t_bwd_out = net(Tq) + net(Tkv) + hbm(3 * (Tq + Tkv))
+    else:
+        t_fwd_in, t_fwd_out, t_bwd_in = hbm(2 * Tkv), hbm(2 * Tq), 0.0
+        t_bwd_out = hbm(3 * (Tq + Tkv))
+    t_a2a = t_fwd_in + t_fwd_out + t_bwd_in + t_bwd_out
     # ring hops: d_cp - 1 KV hops per pass, each beside one attention step
     kv_bytes = 2 * (Hrep // d_hp) * C * d * cal.elem
     t_hop = kv_bytes / (cal.p2p_gbs * 1e9) + cal.launch_s
@@ -86,6 +100,8 @@ def predict(model: ModelConfig, par: ParallelConfig, cal: B200Calibration | None
     t = t_fwd + t_bwd + t_a2a + exposed
     total = 3.5 * 4.0 * S * S * H * d * frac  # algorithmic fwd+bwd FLOPs of the layer
     return {"t_step": t, "t_fwd": t_fwd, "t_bwd": t_bwd, "t_a2a": t_a2a, "t_ring_exposed": exposed,
+            "t_phases": {"fwd.a2a_in": t_fwd_in, "fwd.a2a_out": t_fwd_out, "bwd.a2a_in": t_bwd_in,
+                         "bwd.a2a_out": t_bwd_out},
             "tflops_per_gpu": total / d_sp / t / 1e12, "total_tflops": total / t / 1e12}
 
 

@@ -193,6 +193,20 @@ def test_permute_and_gather_bit_exact():
     assert torch.equal(out.view(torch.int16), x.view(torch.int16)[idx.long()])
 
 
+def test_permute_f32_to_bf16_matches_torch_rounding():
+    """Gradient-gather pack: fp32 -> bf16 (round to nearest even) fused with the
+    [A][B] -> [B][A] block permute; bit-exact vs torch, incl. A = B = 1."""
+    from paper_2406_18485_b200 import kernels as K
+    d = dev()
+    x = torch.randn(4, 3, 40, 16, device=d) * 100
+    y = K.permute_to_bf16(x, 4, 3).view(3, 4, 40, 16)
+    assert torch.equal(y.view(torch.int16), x.permute(1, 0, 2, 3).contiguous().bfloat16().view(torch.int16))
+    z = K.permute_to_bf16(x, 1, 1)
+    assert torch.equal(z.view(torch.int16), x.bfloat16().view(torch.int16))
+    with pytest.raises(ValueError):
+        K.permute_to_bf16(torch.zeros(3, 2, 5, device=d), 3, 2)  # block of 5 values: not a multiple of 8
+
+
 def test_bwd_query_slicing_beyond_one_launch():
     """Query chunks longer than one launch's live list (4096 tiles = 262144
     rows) run as consecutive slices; dK/dV must still sum over all of them."""

@@ -1,5 +1,6 @@
 """B200-calibrated cost model / planner vs measured sweeps. CPU only."""
 
+import json
 import os
 
 import pytest
@@ -58,7 +59,37 @@ def test_enumeration_matches_reference():
 def test_predict_components_sane():
     model = ModelConfig(seq_len=131072, heads=32, kv_heads=32, hidden=4096)
     one = P.predict(model, ParallelConfig(1, 1))
-    assert one["t_a2a"] == 0 and one["t_ring_exposed"] == 0
+    assert one["t_ring_exposed"] == 0 and one["t_a2a"] < 0.01 * one["t_step"]
+    # 1 GPU: only the layout passes remain; measured by tools/trace.py (profiles/r01_trace_1x1w1.json)
+    meas = {"fwd.a2a_in": 0.78e-3, "fwd.a2a_out": 0.35e-3, "bwd.a2a_out": 1.65e-3}
+    for k, v in meas.items():
+        assert abs(one["t_phases"][k] - v) <= 0.25 * v, (k, one["t_phases"][k], v)
+    # 2x2 exchange phases vs the measured trace (profiles/r01_trace_2x2w2.json)
+    two = P.predict(model, ParallelConfig(2, 2, inner_ring=2, placement=Placement.HEAD_FIRST))
+    assert abs(two["t_phases"]["fwd.a2a_in"] - 1.81e-3) <= 0.25 * 1.81e-3
+    assert abs(two["t_phases"]["bwd.a2a_in"] - 0.54e-3) <= 0.25 * 0.54e-3
     ring = P.predict(model, ParallelConfig(1, 8, inner_ring=8, placement=Placement.HEAD_FIRST))
     assert ring["t_ring_exposed"] > 0
     assert 800 < one["tflops_per_gpu"] < 1200
+
+
+def test_trace_export_matches_reference_format(tmp_path):
+    """Measured-trace export uses the reference's Chrome trace schema
+    (ref timeline.py:203-219) and pairs each measured rank with the planner."""
+    from paper_2406_18485_b200 import trace
+    marks = [("fwd.start", 0.0), ("fwd.a2a_in", 1.0), ("fwd.step0", 11.0), ("fwd.step1", 20.0),
+             ("fwd.a2a_out", 21.0), ("bwd.start", 21.5), ("bwd.a2a_in", 22.5), ("bwd.step0", 47.5),
+             ("bwd.step1", 70.0), ("bwd.ring", 70.5), ("bwd.a2a_out", 72.0)]
+    model = ModelConfig(seq_len=131072, heads=32, kv_heads=32, hidden=4096)
+    par = ParallelConfig(d_hp=2, d_cp=2, inner_ring=2, placement=Placement.HEAD_FIRST)
+    path = tmp_path / "t.json"
+    summ = trace.export(str(path), {0: marks, 1: marks}, model, par)
+    recs = json.loads(path.read_text())
+    assert recs and all(set(r) == {"ph", "name", "ts", "dur", "pid", "tid", "args"} for r in recs)
+    assert all(r["ph"] == "X" and r["dur"] >= 0 and "resource" in r["args"] for r in recs)
+    assert {r["pid"] for r in recs} == {0, 1} and {r["tid"] for r in recs} == {0, 1}
+    m = summ["measured_ms"]
+    assert m["fwd.a2a_in"] == 1.0 and m["fwd.ring"] == 19.0 and abs(m["bwd.ring"] - 48.0) < 1e-9
+    assert not any("start" in r["name"] for r in recs)  # the fwd->bwd gap is not a phase
+    p = summ["predicted_ms"]
+    assert p["fwd.ring"] > 0 and p["bwd.ring"] > p["fwd.ring"]
