@@ -30,6 +30,7 @@ compute stream wait (no host sync).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -142,6 +143,21 @@ class Attn2D:
         self._smap = torch.tensor(smap, dtype=torch.int32, device=dev)
         self._dmap_k = torch.tensor(dmap_k, dtype=torch.int32, device=dev)
         self._dmap_v = torch.tensor(dmap_v, dtype=torch.int32, device=dev)
+        # ---- head groups: the HP exchange of group g+1 (and the output gather
+        # of group g) run on NCCL's stream while group g's ring attention runs
+        self.ng = self._choose_groups()
+        self.Hq_g, self.Hk_g = self.Hl // self.ng, self.Hkl // self.ng
+        if self.ng > 1:
+            it = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+            self._qmap, self._kmap, self._kvsrc, self._kvdk, self._kvdv = [], [], [], [], []
+            for g in range(self.ng):
+                self._qmap.append(it([p * self.Hl + g * self.Hq_g + j for p in range(d_hp) for j in range(self.Hq_g)]))
+                self._kmap.append(it([p * self.Hkl + g * self.Hk_g + j for p in range(d_hp) for j in range(self.Hk_g)]))
+                self._kvsrc.append(it([int(src[p * self.Hkl + g * self.Hk_g + j])
+                                       for p in range(d_hp) for j in range(self.Hk_g)]))
+                self._kvdk.append(it([p * 2 * self.Hk_g + j for p in range(d_hp) for j in range(self.Hk_g)]))
+                self._kvdv.append(it([p * 2 * self.Hk_g + self.Hk_g + j for p in range(d_hp) for j in range(self.Hk_g)]))
+            self._iota = it(list(range(d_hp * max(self.Hq_g, self.Hk_g))))
         self._bufs: dict = {}
         self.times = StepTimes()
         self.record_times = False
@@ -150,6 +166,18 @@ class Attn2D:
         # skipped (receive buffers keep pre-staged data). Only for measuring
         # exposed communication (t_layer - t_compute_only, ref timeline.py:152).
         self.comm_enabled = True
+
+    def _choose_groups(self) -> int:
+        """Head groups for the pipelined exchange (1 = one exchange per phase).
+        Opt-in via A2D_HEAD_GROUPS=g: measured on B200 the
+        overlap loses — NCCL's all-to-all kernels take SMs from the attention
+        kernels for longer than the transfer they hide (N=4: 3705 vs 3820
+        TFLOP/s). Needs d_hp > 1, d = 128, no GQA replicas and even splits."""
+        env = os.environ.get("A2D_HEAD_GROUPS")
+        if not env or self.par.d_hp == 1 or self.d != self.bd or self.kd != self.bd or self.rep != 1:
+            return 1
+        g = int(env)
+        return g if g >= 1 and self.Hl % g == 0 and self.Hkl % g == 0 else 1
 
     # ------------------------------------------------------------ helpers
     def _buf(self, name: str, shape, dtype) -> torch.Tensor:
@@ -168,6 +196,48 @@ class Attn2D:
         if not self.comm_enabled:
             return
         dist.all_to_all_single(out, inp, group=self.hp_group)
+
+    def _a2a_async(self, out: torch.Tensor, inp: torch.Tensor):
+        """All-to-all on NCCL's stream; the caller waits (stream-orders) later."""
+        if not self.comm_enabled:
+            return None
+        return dist.all_to_all_single(out, inp, group=self.hp_group, async_op=True)
+
+    # ---- grouped exchange (ng > 1): packs / unpacks of head group g
+    def _send_q_g(self, x: torch.Tensor, g: int, name: str, tm: bool) -> torch.Tensor:
+        """[d_hp][Hq_g][L][d] bf16 send buffer of query-like tensor x for group g."""
+        d_hp, dk = self.par.d_hp, self.bd
+        send = self._buf(f"{name}.send{g}", (d_hp, self.Hq_g, self.L, dk), torch.bfloat16)
+        if tm and x.dtype == torch.bfloat16 and x.stride(-1) == 1:
+            K.copy_rows(x, send.view(d_hp * self.Hq_g, self.L, dk).transpose(0, 1), self._qmap[g])
+        else:
+            x = K.pad_dim(x.transpose(0, 1) if tm else x, dk)
+            K.gather_blocks(x, self._qmap[g], send)
+        return send
+
+    def _send_kv_g(self, k: torch.Tensor, v: torch.Tensor, g: int, tm: bool) -> torch.Tensor:
+        d_hp, dk = self.par.d_hp, self.bd
+        send = self._buf(f"kv.send{g}", (d_hp, 2, self.Hk_g, self.L, dk), torch.bfloat16)
+        if tm and k.dtype == v.dtype == torch.bfloat16 and k.stride(-1) == 1 and v.stride(-1) == 1:
+            rows = send.view(d_hp * 2 * self.Hk_g, self.L, dk).transpose(0, 1)
+            K.copy_rows(k, rows, self._kvsrc[g], self._kvdk[g])
+            K.copy_rows(v, rows, self._kvsrc[g], self._kvdv[g])
+        else:
+            if tm:
+                k, v = k.transpose(0, 1), v.transpose(0, 1)
+            k, v = K.pad_dim(k, dk), K.pad_dim(v, dk)
+            K.gather_blocks(k, self._kvsrc[g], send, self._kvdk[g])
+            K.gather_blocks(v, self._kvsrc[g], send, self._kvdv[g])
+        return send
+
+    def _unpack_g(self, recv: torch.Tensor, hmap: torch.Tensor, out: torch.Tensor, tm: bool) -> None:
+        """recv [d_hp][Hn][L][d] -> the caller's SeqSharded tensor at heads hmap."""
+        n = recv.shape[0] * recv.shape[1]
+        flat = recv.view(n, self.L, recv.shape[-1])
+        if tm:
+            K.copy_rows(flat.transpose(0, 1), out, None, hmap)
+        else:
+            K.gather_blocks(flat, self._iota[:n], out, hmap)
 
     def _new(self, name: str, shape, dtype, fresh: bool) -> torch.Tensor:
         """Workspace buffer, or newly allocated memory when the result outlives the call."""
@@ -274,19 +344,21 @@ class Attn2D:
     @staticmethod
     def _wait(works):
         for wk in works or ():
-            wk.wait()
+            if wk is not None:
+                wk.wait()
 
     # ------------------------------------------------------------ ring forward
-    def _ring_forward(self, qh, kv_own, out_h, lse):
+    def _ring_forward(self, qh, kv_own, out_h, lse, mark: bool = True):
         d_cp, w = self.par.d_cp, self.par.inner_ring
         qplan = self.plans[self.cp]
         kd = qh.shape[-1]
         if d_cp == 1:
             K.fwd_chunk(qh, kv_own[0], kv_own[1], qplan, self.plans[self.cp], self.causal, self.scale,
                         lse, None, out_h)
-            self._mark("fwd.step0")
+            if mark:
+                self._mark("fwd.step0")
             return
-        acc = self._buf("fwd.acc", (self.Hl, self.C, kd), torch.float32)
+        acc = self._buf("fwd.acc", (qh.shape[0], self.C, kd), torch.float32)
         inner = [self._buf(f"kv.in{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
         outer = [self._buf(f"kv.out{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
         cur, first = kv_own, kv_own
@@ -305,7 +377,8 @@ class Attn2D:
             last = s == d_cp - 1
             K.fwd_chunk(qh, cur[0], cur[1], qplan, self.plans[step.source], self.causal, self.scale, lse, acc,
                         out_h if last else None, merge=s > 0)
-            self._mark(f"fwd.step{s}")
+            if mark:
+                self._mark(f"fwd.step{s}")
             if t + 1 < w:
                 self._wait(w_in)
                 cur = nxt_inner
@@ -314,15 +387,16 @@ class Attn2D:
                 cur = first = nxt_outer
 
     # ------------------------------------------------------------ ring backward
-    def _ring_backward(self, qh, kv_own, doh, lse2, delta, dq_acc):
+    def _ring_backward(self, qh, kv_own, doh, lse2, delta, dq_acc, mark: bool = True):
         d_cp, w = self.par.d_cp, self.par.inner_ring
         qplan = self.plans[self.cp]
-        shape = (2, self.Hkl, self.C, self.bd)
+        shape = (2, kv_own.shape[1], self.C, self.bd)
         if d_cp == 1:
             dkv = self._buf("bwd.dkv_home", shape, torch.float32)
             K.bwd_chunk(qh, kv_own[0], kv_own[1], doh, qplan, self.plans[self.cp], lse2, delta, dq_acc,
                         dkv[0], dkv[1], False, self.causal, self.scale)
-            self._mark("bwd.step0")
+            if mark:
+                self._mark("bwd.step0")
             return dkv
         part = self._buf("bwd.part", shape, torch.float32)
         acc = [self._buf(f"bwd.acc{i}", shape, torch.float32) for i in range(2)]
@@ -348,7 +422,8 @@ class Attn2D:
             if s > 0:
                 self._wait(w_dkv)            # accumulator of this chunk arrived in acc[s % 2]
                 K.add_(acc[s % 2], part)     # K4: accumulate ...
-            self._mark(f"bwd.step{s}")
+            if mark:
+                self._mark(f"bwd.step{s}")
             # ... and forward: next consumer is (r, p+1) inside an outer step, (r+1, p+1) across
             last = s == d_cp - 1
             dst = home if last else acc[(s + 1) % 2]
@@ -381,18 +456,73 @@ class Attn2D:
             raise ValueError(f"layout must be 'hld' or 'lhd', got {layout!r}")
         return layout == "lhd"
 
+    def _scatter_grouped(self, q, k, v, tm: bool):
+        """Issue every head group's q/kv all-to-all (NCCL stream) up front.
+        Returns (qh, kvh, waits): qh (Hl, C, d) and kvh (ng, 2, Hk_g, C, d) are
+        filled group by group by finish(g), which stream-orders on the group's
+        transfer and unpacks it."""
+        d_hp, dk = self.par.d_hp, self.bd
+        qh = torch.empty((self.Hl, self.C, dk), dtype=torch.bfloat16, device=self.device)
+        kvh = torch.empty((self.ng, 2, self.Hk_g, self.C, dk), dtype=torch.bfloat16, device=self.device)
+        pend = []
+        for g in range(self.ng):
+            sq, skv = self._send_q_g(q, g, "q", tm), self._send_kv_g(k, v, g, tm)
+            rq = self._buf(f"q.recv{g}", sq.shape, torch.bfloat16)
+            rkv = self._buf(f"kv.recv{g}", skv.shape, torch.bfloat16)
+            pend.append((rq, rkv, self._a2a_async(rq, sq), self._a2a_async(rkv, skv)))
+
+        def finish(g):
+            rq, rkv, wq, wkv = pend[g]
+            self._wait([wq, wkv])
+            lo = g * self.Hq_g
+            K.permute_blocks(rq, d_hp, self.Hq_g, out=qh[lo:lo + self.Hq_g])
+            K.permute_blocks(rkv, d_hp, 2 * self.Hk_g, out=kvh[g])
+        return qh, kvh, finish
+
     def scatter_inputs(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld"):
         """SeqSharded q, k, v -> HeadSharded (qh, kvh) in memory they own (ref
-        seq_alltoall_scatter + kv_replicate, sharding.py:109-152)."""
+        seq_alltoall_scatter + kv_replicate, sharding.py:109-152); kvh is
+        (ng, 2, Hk_g, C, d), head group major."""
         tm = self._layout(layout)
         self._check_inputs(q, k, v, tm)
+        if self.ng > 1:
+            qh, kvh, finish = self._scatter_grouped(q, k, v, tm)
+            for g in range(self.ng):
+                finish(g)
+            return qh, kvh
         kd = self.kd
-        return self._scatter_q(q, "q", kd, tm, fresh=True), self._scatter_kv(k, v, "kv", kd, tm, fresh=True)
+        return (self._scatter_q(q, "q", kd, tm, fresh=True),
+                self._scatter_kv(k, v, "kv", kd, tm, fresh=True).unsqueeze(0))
+
+    def _out_tensor(self, heads: int, tm: bool) -> torch.Tensor:
+        shape = (self.L, heads, self.d) if tm else (heads, self.L, self.d)
+        return torch.empty(shape, dtype=torch.bfloat16, device=self.device)
 
     def gather_output(self, out_h: torch.Tensor, layout: str = "hld") -> torch.Tensor:
         """HeadSharded O -> SeqSharded O in the caller's layout (ref seq_alltoall_gather)."""
         tm = self._layout(layout)
+        if self.ng > 1:
+            out = self._out_tensor(self.model.heads, tm)
+            for g in range(self.ng):
+                r = self._gather_g(out_h[g * self.Hq_g:(g + 1) * self.Hq_g], "out", g, False)
+                self._unpack_g(*r, self._qmap[g], out, tm)
+            return out
         return self._to_layout(self._gather(out_h, "out", fresh=not tm), tm)
+
+    def _gather_g(self, x: torch.Tensor, name: str, g: int, from_f32: bool, wait: bool = True):
+        """Head group g of a HeadSharded tensor (Hn, C, d) -> (recv [d_hp][Hn][L][d] bf16, Work)."""
+        d_hp, Hn = self.par.d_hp, x.shape[0]
+        send = self._buf(f"{name}.gsend{g}", (d_hp, Hn, self.L, x.shape[-1]), torch.bfloat16)
+        if from_f32:
+            K.permute_to_bf16(x, Hn, d_hp, out=send)
+        else:
+            K.permute_blocks(x, Hn, d_hp, out=send)
+        recv = self._buf(f"{name}.grecv{g}", send.shape, torch.bfloat16)
+        w = self._a2a_async(recv, send)
+        if wait:
+            self._wait([w])
+            return (recv,)
+        return recv, w
 
     def forward_with_state(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld"):
         """forward() returning (out, state); state = (qh, kvh, out_h, lse) owns its
@@ -402,6 +532,26 @@ class Attn2D:
         self.times.clear()
         self._mark("fwd.start")
         kd = self.kd
+        if self.ng > 1:
+            # pipelined: group g's ring overlaps group g+1's input exchange and
+            # group g-1's output exchange
+            qh, kvh, finish = self._scatter_grouped(q, k, v, tm)
+            out_h = torch.empty((self.Hl, self.C, kd), dtype=torch.bfloat16, device=self.device)
+            lse = torch.empty((self.Hl, self.C), dtype=torch.float32, device=self.device)
+            out = self._out_tensor(self.model.heads, tm)
+            pend = []
+            for g in range(self.ng):
+                finish(g)
+                if g == 0:
+                    self._mark("fwd.a2a_in")
+                sl = slice(g * self.Hq_g, (g + 1) * self.Hq_g)
+                self._ring_forward(qh[sl], kvh[g], out_h[sl], lse[sl], mark=g == self.ng - 1)
+                pend.append(self._gather_g(out_h[sl], "out", g, False, wait=False))
+            for g, (recv, w) in enumerate(pend):
+                self._wait([w])
+                self._unpack_g(recv, self._qmap[g], out, tm)
+            self._mark("fwd.a2a_out")
+            return out, (qh, kvh, out_h, lse)
         qh = self._scatter_q(q, "q", kd, tm, fresh=True)
         kvh = self._scatter_kv(k, v, "kv", kd, tm, fresh=True)
         self._mark("fwd.a2a_in")
@@ -410,7 +560,7 @@ class Attn2D:
         self._ring_forward(qh, kvh, out_h, lse)
         out = self._gather(out_h, "out", fresh=not tm)
         self._mark("fwd.a2a_out")
-        return self._to_layout(out, tm), (qh, kvh, out_h, lse)
+        return self._to_layout(out, tm), (qh, kvh.unsqueeze(0), out_h, lse)
 
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld") -> torch.Tensor:
         """This rank's SeqSharded chunk -> SeqSharded output, bf16.
@@ -434,6 +584,9 @@ class Attn2D:
         qh, kvh, out_h, lse = state
         self._mark("bwd.start")
         bd = self.bd
+        if self.ng > 1:
+            return self._backward_grouped(dout, tm, qh, kvh, out_h, lse)
+        kvh = kvh[0]
         if self.kd != bd:  # head dim <= 64: the backward kernel runs at 128 (exact zero padding)
             qh, kvh, out_h = K.pad_dim(qh, bd), K.pad_dim(kvh, bd), K.pad_dim(out_h, bd)
         out_b = out_h
@@ -454,6 +607,43 @@ class Attn2D:
             dv = K.to_bf16(K.sum_replicas(self._gather(dkv[1], "dv32"), self.rep))
         self._mark("bwd.a2a_out")
         return self._to_layout(dq, tm), self._to_layout(dk, tm), self._to_layout(dv, tm)
+
+    def _backward_grouped(self, dout, tm, qh, kvh, out_h, lse):
+        """Pipelined backward: every group's dO all-to-all is issued up front;
+        group g's gradient gather (fp32 -> bf16 fused into the pack) runs on
+        NCCL's stream while group g+1's ring backward computes."""
+        d_hp, bd = self.par.d_hp, self.bd
+        pend_in = []
+        for g in range(self.ng):
+            sd = self._send_q_g(dout, g, "do", tm)
+            rd = self._buf(f"do.recv{g}", sd.shape, torch.bfloat16)
+            pend_in.append((rd, self._a2a_async(rd, sd)))
+        dq = self._out_tensor(self.model.heads, tm)
+        dk = self._out_tensor(self.H_rep, tm)
+        dv = self._out_tensor(self.H_rep, tm)
+        pend_out = []
+        for g in range(self.ng):
+            rd, w = pend_in[g]
+            self._wait([w])
+            doh = self._buf("doh", (self.Hq_g, self.C, bd), torch.bfloat16)
+            K.permute_blocks(rd, d_hp, self.Hq_g, out=doh)
+            if g == 0:
+                self._mark("bwd.a2a_in")
+            sl = slice(g * self.Hq_g, (g + 1) * self.Hq_g)
+            lse2, delta = K.bwd_preprocess(out_h[sl], doh, lse[sl])
+            dq_acc = self._buf("dq_acc", (self.Hq_g, self.C, bd), torch.float32)
+            dq_acc.zero_()
+            dkv = self._ring_backward(qh[sl], kvh[g], doh, lse2, delta, dq_acc, mark=g == self.ng - 1)
+            for name, src, dst, hmap in (("dq", dq_acc, dq, self._qmap[g]), ("dk", dkv[0], dk, self._kmap[g]),
+                                         ("dv", dkv[1], dv, self._kmap[g])):
+                recv, w = self._gather_g(src, name, g, True, wait=False)
+                pend_out.append((recv, w, hmap, dst))
+        self._mark("bwd.ring")
+        for recv, w, hmap, dst in pend_out:
+            self._wait([w])
+            self._unpack_g(recv, hmap, dst, tm)
+        self._mark("bwd.a2a_out")
+        return dq, dk, dv
 
     def flops(self) -> float:
         """Algorithmic fwd+bwd FLOPs of the whole layer (all ranks): 3.5 x 4 S^2 H d x (1/2 if causal)."""

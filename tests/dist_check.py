@@ -104,6 +104,7 @@ def main():
             rq, rk, rv = orc.attention_grads(qb, kb, vb, dob, pos, pos, bool(a.causal))
             res["dQ"], res["dK"], res["dV"] = metrics(DQ, rq), metrics(DK, rk), metrics(DV, rv)
         res["config"] = vars(a)
+        res["head_groups"] = op.ng
         print(json.dumps(res))
         if a.out:
             with open(a.out, "w") as f:

@@ -34,12 +34,13 @@ CASES = [
 ]
 
 
-def _run(nproc, args, tmp_path):
+def _run(nproc, args, tmp_path, env=None):
     out = tmp_path / "res.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "dist_check.py"),
            *args, "--out", str(out)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return json.loads(out.read_text())
 
@@ -93,16 +94,17 @@ def test_dist_token_major_fused_qkv_autograd(case, tmp_path):
             f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
 
 
-SCPP = [(1, 1, 1), (2, 1, 1), (1, 2, 2), (2, 2, 1)]
+SCPP = [(1, 1, 1), (2, 1, 1), (1, 2, 2), (2, 2, 1), (2, 2, 2, "groups")]
 
 
-@pytest.mark.parametrize("case", SCPP, ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("case", SCPP, ids=lambda c: "x".join(map(str, c[:3])) + ("-groups" if len(c) > 3 else ""))
 def test_selective_checkpoint_pp(case, tmp_path):
     """SC++ (SURVEY §8f row 2): checkpointed layers recompute everything except
     the whitelisted 2D attention, whose O/LSE are kept — same gradients as plain
     autograd, no attention-forward kernel in the backward pass, while
     torch.utils.checkpoint re-runs the ring forward."""
-    d_hp, d_cp, w = case
+    d_hp, d_cp, w = case[:3]
+    grouped = len(case) > 3  # pipelined head groups (A2D_HEAD_GROUPS=2, GQA 8/4)
     n = d_hp * d_cp
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
@@ -110,7 +112,10 @@ def test_selective_checkpoint_pp(case, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "tests", "scpp_check.py"),
            "--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--out", str(out)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    if grouped:
+        cmd += ["--kv-heads", "4"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env={**os.environ, "A2D_HEAD_GROUPS": "2"} if grouped else None)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for res in json.loads(out.read_text()):
         assert res["grad_rel_l2"] <= 1e-2, res
@@ -118,3 +123,31 @@ def test_selective_checkpoint_pp(case, tmp_path):
         k = res["fwd_kernels_in_bwd"]
         assert k["plain"] == 0 and k["scpp"] == 0, res
         assert k["torch_checkpoint"] >= 2 * d_cp, res  # 2 layers x d_cp ring steps recomputed
+
+
+GROUPED = [
+    # d_hp, d_cp, w, placement, H, H_kv, S, d, fused-qkv
+    (2, 1, 1, "head_first", 8, 8, 1024, 128, False),
+    (2, 2, 2, "head_first", 8, 4, 2048, 128, False),   # GQA inside each head group
+    (4, 1, 1, "context_first", 8, 8, 1024, 128, True),  # token-major fused QKV views
+    (2, 2, 1, "context_first", 8, 8, 2048, 128, True),
+]
+
+
+@pytest.mark.parametrize("case", GROUPED, ids=lambda c: "x".join(map(str, c[:3])) + f"-{c[3]}-H{c[4]}-{c[5]}"
+                         + ("-lhd" if c[8] else ""))
+def test_dist_pipelined_head_groups(case, tmp_path):
+    """Head-group pipelined exchange (A2D_HEAD_GROUPS=2): group g+1's all-to-all
+    overlaps group g's ring; same parity bar as the one-shot exchange."""
+    d_hp, d_cp, w, pl, H, Hkv, S, d, fused = case
+    n = d_hp * d_cp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    args = ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
+            "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", str(d)]
+    res = _run(n, args + (["--fused-qkv"] if fused else []), tmp_path, env={"A2D_HEAD_GROUPS": "2"})
+    assert res["head_groups"] == 2
+    for name in ("O", "dQ", "dK", "dV"):
+        ma, rl, rng = res[name]
+        assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
+            f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
