@@ -159,6 +159,13 @@ class Attn2D:
                 self._kvdv.append(it([p * 2 * self.Hk_g + self.Hk_g + j for p in range(d_hp) for j in range(self.Hk_g)]))
             self._iota = it(list(range(d_hp * max(self.Hq_g, self.Hk_g))))
         self._bufs: dict = {}
+        # ---- HP exchange transport: "symm" = copy-engine writes into the peers'
+        # symmetric-memory buffers + a device barrier (no SMs taken, ~770 GB/s
+        # per direction); "nccl" = all_to_all_single. A2D_TRANSPORT overrides.
+        self.transport = "nccl"
+        self._symm = None
+        if d_hp > 1 and os.environ.get("A2D_TRANSPORT", "symm") == "symm":
+            self._init_symm()
         self.times = StepTimes()
         self.record_times = False
         self.saved = None
@@ -166,6 +173,88 @@ class Attn2D:
         # skipped (receive buffers keep pre-staged data). Only for measuring
         # exposed communication (t_layer - t_compute_only, ref timeline.py:152).
         self.comm_enabled = True
+
+    def _init_symm(self) -> None:
+        """Symmetric buffer of this HP group: IN region (scatters: q + kv, or
+        dO) and OUT region (gathers: O, or dQ + dK + dV, fp32 when GQA replicas
+        are summed after the gather). Collective over the HP group."""
+        try:
+            import torch.distributed._symmetric_memory as symm
+        except ImportError:
+            return
+        d_hp, tok = self.par.d_hp, self.L * self.bd
+        self._in_bytes = d_hp * tok * 2 * (self.Hl + 2 * self.Hkl)
+        out_bytes = d_hp * tok * (2 * self.Hl + 4 * 2 * self.Hkl)
+        buf = symm.empty(self._in_bytes + out_bytes, dtype=torch.uint8, device=self.device)
+        self._symm = symm.rendezvous(buf, self.hp_group.group_name)
+        self._symm_buf = buf
+        self._peer = [self._symm.get_buffer(r, (buf.numel(),), torch.uint8) for r in range(d_hp)]
+        self._xstreams = [torch.cuda.Stream(self.device) for _ in range(d_hp - 1)]
+        self._xstream_bar = torch.cuda.Stream(self.device)
+        self.transport = "symm"
+
+    # byte offsets of each exchange inside the symmetric buffer (static layout:
+    # a region is only rewritten after every peer passed a later barrier)
+    def _xoff(self, name: str, g: int = 0) -> int:
+        d_hp, tok = self.par.d_hp, self.L * self.bd
+        q_bytes = d_hp * tok * 2 * self.Hq_g   # one head group of a query-like tensor
+        kv_bytes = d_hp * tok * 2 * 2 * self.Hk_g
+        k_bytes = d_hp * tok * 2 * self.Hk_g
+        ng = self.ng
+        if name in ("q", "do"):
+            return g * q_bytes
+        if name == "kv":
+            return ng * q_bytes + g * kv_bytes
+        base = self._in_bytes
+        if name in ("out", "dq"):
+            return base + g * q_bytes
+        if name in ("dk", "dv"):
+            return base + ng * q_bytes + (0 if name == "dk" else ng * k_bytes) + g * k_bytes
+        if name in ("dk32", "dv32"):  # fp32, ng == 1
+            return base + q_bytes + (0 if name == "dk32" else 2 * k_bytes)
+        raise KeyError(name)
+
+    def _xchg(self, send: torch.Tensor, name: str, g: int = 0, wait: bool = True):
+        """All-to-all of send [d_hp][...] -> recv [d_hp][...] (recv[p] = peer p's
+        send[me]). "symm": one copy-engine write per peer straight into its
+        buffer, then a device barrier. Returns recv (and, wait=False, an event
+        the consumer stream must wait for)."""
+        if self.transport != "symm":
+            recv = self._buf(f"{name}.recv{g}", send.shape, send.dtype)
+            w = None
+            if self.comm_enabled:
+                w = dist.all_to_all_single(recv, send, group=self.hp_group, async_op=not wait)
+            return recv if wait else (recv, w)
+        d_hp, me = self.par.d_hp, self.hp
+        nb = send[0].numel() * send.element_size()
+        off = self._xoff(name, g)
+        recv = self._symm_buf[off:off + d_hp * nb].view(send.dtype).view(send.shape)
+        main = torch.cuda.current_stream()
+        bar = self._xstream_bar
+        src = send.view(torch.uint8).view(d_hp, nb)
+        if self.comm_enabled:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            for i in range(d_hp - 1):
+                p = (me + 1 + i) % d_hp
+                s = self._xstreams[i]
+                s.wait_event(ev)
+                with torch.cuda.stream(s):
+                    self._peer[p][off + me * nb:off + (me + 1) * nb].copy_(src[p], non_blocking=True)
+                bar.wait_stream(s)
+        else:
+            bar.wait_stream(main)
+        with torch.cuda.stream(bar):
+            bar.wait_stream(main)
+            recv[me].copy_(send[me], non_blocking=True)
+            if self.comm_enabled:
+                self._symm.barrier()
+        done = torch.cuda.Event()
+        done.record(bar)
+        if wait:
+            main.wait_event(done)
+            return recv
+        return recv, done
 
     def _choose_groups(self) -> int:
         """Head groups for the pipelined exchange (1 = one exchange per phase).
@@ -191,17 +280,6 @@ class Attn2D:
     def _mark(self, name):
         if self.record_times:
             self.times.mark(name)
-
-    def _a2a(self, out: torch.Tensor, inp: torch.Tensor):
-        if not self.comm_enabled:
-            return
-        dist.all_to_all_single(out, inp, group=self.hp_group)
-
-    def _a2a_async(self, out: torch.Tensor, inp: torch.Tensor):
-        """All-to-all on NCCL's stream; the caller waits (stream-orders) later."""
-        if not self.comm_enabled:
-            return None
-        return dist.all_to_all_single(out, inp, group=self.hp_group, async_op=True)
 
     # ---- grouped exchange (ng > 1): packs / unpacks of head group g
     def _send_q_g(self, x: torch.Tensor, g: int, name: str, tm: bool) -> torch.Tensor:
@@ -265,8 +343,7 @@ class Attn2D:
         x = self._head_major_send(x, name, dk, token_major, fresh and d_hp == 1)
         if d_hp == 1:
             return x
-        recv = self._buf(name + ".recv", (d_hp, self.Hl, self.L, dk), torch.bfloat16)
-        self._a2a(recv, x)
+        recv = self._xchg(x.view(d_hp, self.Hl, self.L, dk), name)
         out = self._new(name, (self.Hl, self.C, dk), torch.bfloat16, fresh)
         return K.permute_blocks(recv, d_hp, self.Hl, out=out)
 
@@ -289,8 +366,7 @@ class Attn2D:
             K.gather_blocks(v, self._smap, send, self._dmap_v)
         if d_hp == 1:
             return send.view(2, self.Hkl, self.C, dk)
-        recv = self._buf(name + ".recv", (d_hp, 2, self.Hkl, self.L, dk), torch.bfloat16)
-        self._a2a(recv, send)
+        recv = self._xchg(send, name)
         out = self._new(name, (2, self.Hkl, self.C, dk), torch.bfloat16, fresh)
         return K.permute_blocks(recv, d_hp, 2 * self.Hkl, out=out)
 
@@ -303,11 +379,9 @@ class Attn2D:
         B = x.shape[0]
         send = self._buf(name + ".send", (d_hp, B) + (self.L,) + tuple(x.shape[2:]), x.dtype)
         K.permute_blocks(x.contiguous(), B, d_hp, out=send)
+        recv = self._xchg(send, name)
         if fresh:
-            recv = torch.empty(send.shape, dtype=x.dtype, device=x.device)
-        else:
-            recv = self._buf(name + ".recv", send.shape, x.dtype)
-        self._a2a(recv, send)
+            recv = recv.clone()
         return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
 
     def _gather_f32(self, x: torch.Tensor, name: str, fresh: bool = False) -> torch.Tensor:
@@ -319,8 +393,9 @@ class Attn2D:
             return K.permute_to_bf16(x, 1, 1, out=self._new(name + ".bf16", x.shape, torch.bfloat16, fresh))
         send = self._buf(name + ".send", (d_hp, B, self.L) + tuple(x.shape[2:]), torch.bfloat16)
         K.permute_to_bf16(x, B, d_hp, out=send)
-        recv = self._new(name + ".recv", send.shape, torch.bfloat16, fresh)
-        self._a2a(recv, send)
+        recv = self._xchg(send, name)
+        if fresh:
+            recv = recv.clone()
         return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
 
     def _to_layout(self, x: torch.Tensor, token_major: bool) -> torch.Tensor:
@@ -343,8 +418,13 @@ class Attn2D:
 
     @staticmethod
     def _wait(works):
+        """Stream-order the current stream after NCCL works / CUDA events."""
         for wk in works or ():
-            if wk is not None:
+            if wk is None:
+                continue
+            if isinstance(wk, torch.cuda.Event):
+                torch.cuda.current_stream().wait_event(wk)
+            else:
                 wk.wait()
 
     # ------------------------------------------------------------ ring forward
@@ -467,9 +547,9 @@ class Attn2D:
         pend = []
         for g in range(self.ng):
             sq, skv = self._send_q_g(q, g, "q", tm), self._send_kv_g(k, v, g, tm)
-            rq = self._buf(f"q.recv{g}", sq.shape, torch.bfloat16)
-            rkv = self._buf(f"kv.recv{g}", skv.shape, torch.bfloat16)
-            pend.append((rq, rkv, self._a2a_async(rq, sq), self._a2a_async(rkv, skv)))
+            rq, wq = self._xchg(sq, "q", g, wait=False)
+            rkv, wkv = self._xchg(skv, "kv", g, wait=False)
+            pend.append((rq, rkv, wq, wkv))
 
         def finish(g):
             rq, rkv, wq, wkv = pend[g]
@@ -517,8 +597,7 @@ class Attn2D:
             K.permute_to_bf16(x, Hn, d_hp, out=send)
         else:
             K.permute_blocks(x, Hn, d_hp, out=send)
-        recv = self._buf(f"{name}.grecv{g}", send.shape, torch.bfloat16)
-        w = self._a2a_async(recv, send)
+        recv, w = self._xchg(send, name, g, wait=False)
         if wait:
             self._wait([w])
             return (recv,)
@@ -616,8 +695,7 @@ class Attn2D:
         pend_in = []
         for g in range(self.ng):
             sd = self._send_q_g(dout, g, "do", tm)
-            rd = self._buf(f"do.recv{g}", sd.shape, torch.bfloat16)
-            pend_in.append((rd, self._a2a_async(rd, sd)))
+            pend_in.append(self._xchg(sd, "do", g, wait=False))
         dq = self._out_tensor(self.model.heads, tm)
         dk = self._out_tensor(self.H_rep, tm)
         dv = self._out_tensor(self.H_rep, tm)

@@ -33,6 +33,8 @@ class B200Calibration:
     bwd_tflops: float = 940.0      # backward chunk kernel in a full step (kbench alone: 980)
     short_chunk_tokens: float = 500.0   # kernel efficiency ~ C / (C + this) for small chunks
     a2a_gbs: float = 620.0         # NCCL all_to_all_single: time ~ whole buffer / this (traces, d_hp = 2 and 4)
+    ce_gbs: float = 770.0          # copy-engine write into a peer's symmetric buffer (tools/probes/peer_probe.py)
+    transport: str = "symm"        # dist.Attn2D default; "nccl" for the round-1 sweeps
     p2p_gbs: float = 770.0         # per-direction peer bandwidth (B200 profiling guide)
     hbm_gbs: float = 6527.5        # MEASURED_PEAKS hbm_gbs (K4 add)
     pack_gbs: float = 5500.0       # achieved by the pack / permute / convert kernels (traces)
@@ -71,7 +73,11 @@ def predict(model: ModelConfig, par: ParallelConfig, cal: B200Calibration | None
     Tkv = 2 * Hrep * L * d * cal.elem       # k and v after replication
     hbm = lambda b: b / (cal.pack_gbs * 1e9)  # noqa: E731
     if d_hp > 1:
-        net = lambda b: b / (cal.a2a_gbs * 1e9) + cal.launch_s  # noqa: E731
+        if cal.transport == "nccl":
+            net = lambda b: b / (cal.a2a_gbs * 1e9) + cal.launch_s  # noqa: E731
+        else:  # crossing bytes on the copy engines + the local chunk copy + a device barrier
+            net = lambda b: (b * (d_hp - 1) / d_hp / (cal.ce_gbs * 1e9) + hbm(2 * b / d_hp)  # noqa: E731
+                             + 2 * cal.launch_s)
         t_fwd_in = net(Tq) + net(Tkv) + hbm(2 * Tkv + 2 * (Tq + Tkv))   # kv pack, unpack permutes
         t_fwd_out = net(Tq) + hbm(2 * Tq)
         t_bwd_in = net(Tq) + hbm(2 * Tq)
@@ -138,7 +144,9 @@ def plan(model: ModelConfig, n_gpus: int, cal: B200Calibration | None = None, ca
 
 
 def check_against_sweep(path: str, cal: B200Calibration | None = None) -> dict:
-    """Compare predictions with a measured sweep (tools/sweep.py JSONL)."""
+    """Compare predictions with a measured sweep (tools/sweep.py JSONL; the
+    round-1 sweeps ran the NCCL transport)."""
+    cal = cal or B200Calibration(transport="nccl")
     errs, pairs = [], []
     for line in open(path):
         r = json.loads(line)

@@ -30,7 +30,7 @@ def test_planner_pick_is_near_measured_best(path):
         groups.setdefault((s["seq"], s["n"]), []).append((rec["ms_per_step"], s))
     for (seq, n), rows in groups.items():
         model = ModelConfig(seq_len=seq, heads=32, kv_heads=32, hidden=4096)
-        _, pick = P.plan(model, n)[0]
+        _, pick = P.plan(model, n, P.B200Calibration(transport="nccl"))[0]
         meas = {(s["d_hp"], s["d_cp"], s["w"], s["placement"]): t for t, s in rows}
         t_pick = meas[(pick.d_hp, pick.d_cp, pick.inner_ring, pick.placement.value)]
         assert t_pick <= 1.03 * min(meas.values()), (seq, n, pick, t_pick, min(meas.values()))
@@ -65,9 +65,14 @@ def test_predict_components_sane():
     for k, v in meas.items():
         assert abs(one["t_phases"][k] - v) <= 0.25 * v, (k, one["t_phases"][k], v)
     # 2x2 exchange phases vs the measured trace (profiles/r01_trace_2x2w2.json)
-    two = P.predict(model, ParallelConfig(2, 2, inner_ring=2, placement=Placement.HEAD_FIRST))
+    par = ParallelConfig(2, 2, inner_ring=2, placement=Placement.HEAD_FIRST)
+    two = P.predict(model, par, P.B200Calibration(transport="nccl"))
     assert abs(two["t_phases"]["fwd.a2a_in"] - 1.81e-3) <= 0.25 * 1.81e-3
     assert abs(two["t_phases"]["bwd.a2a_in"] - 0.54e-3) <= 0.25 * 0.54e-3
+    # symmetric-memory transport (profiles/r01_trace_symm_2x2w2.json): 1.35 / 0.33 ms
+    sym = P.predict(model, par)
+    assert abs(sym["t_phases"]["fwd.a2a_in"] - 1.35e-3) <= 0.25 * 1.35e-3
+    assert abs(sym["t_phases"]["bwd.a2a_in"] - 0.33e-3) <= 0.35 * 0.33e-3
     ring = P.predict(model, ParallelConfig(1, 8, inner_ring=8, placement=Placement.HEAD_FIRST))
     assert ring["t_ring_exposed"] > 0
     assert 800 < one["tflops_per_gpu"] < 1200
