@@ -128,7 +128,8 @@ A2D_DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_clus
 }
 
 // ------------------------------------------------------------------ tcgen05
-// CTA-pair (cta_group::2) variants: the same warp id of both CTAs allocates /
+// CTA-pair (cta_group::2) variants — validated on B200 by the pair forward
+// experiment; building blocks for a pair backward. The same warp id of both CTAs allocates /
 // deallocates; only the leader CTA issues MMAs, which read A rows [0,128) and
 // B columns [0,N/2) from the leader's smem/TMEM and the rest from the peer's
 // (same addresses), and write D rows [0,128) / [128,256) to each CTA's TMEM.
@@ -203,9 +204,8 @@ A2D_DEV void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t 
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// Warp-uniform issue: the whole warp executes these (so operands stay in
-// uniform registers and no per-lane waterfall loop is generated) and only the
-// lane with `issue` != 0 (from elect_one()) actually issues.
+// Warp-uniform issue: the whole (converged) warp computes descriptors in
+// uniform registers and one elected lane issues inside `if (elect_one())`.
 A2D_DEV uint32_t elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -215,35 +215,6 @@ A2D_DEV uint32_t elect_one() {
       : "=r"(pred));
   return pred;
 }
-A2D_DEV void umma_ss_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate,
-                       uint32_t issue) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "setp.ne.b32 q, %5, 0;\n\t"
-      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(issue)
-      : "memory");
-}
-A2D_DEV void umma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate,
-                       uint32_t issue) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "setp.ne.b32 q, %5, 0;\n\t"
-      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(issue)
-      : "memory");
-}
-A2D_DEV void umma_commit_w(uint64_t* bar, uint32_t issue) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\t"
-      "setp.ne.b32 q, %1, 0;\n\t"
-      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)),
-      "r"(issue)
-      : "memory");
-}
-
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
 A2D_DEV void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -338,19 +309,10 @@ A2D_DEV float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA/ALU pipes (offloads the MUFU unit): round-to-nearest split
-// x = n + f, f in [-0.5, 0.5], degree-3 near-minimax polynomial for 2^f (max
-// relative error 1.3e-4, below bf16's half ulp), exponent added as an integer.
-A2D_DEV float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = __fadd_rn(x, 12582912.f);  // 1.5 * 2^23: round(x) lands in the low mantissa bits
-  const float r = __fadd_rn(t, -12582912.f);
-  const float f = __fadd_rn(x, -r);
-  const float p = fmaf(fmaf(fmaf(0.054006658f, f, 0.24244328f), f, 0.69344431f), f, 0.99994266f);
-  const int n = __float_as_int(t) - 0x4B400000;
-  return __int_as_float(__float_as_int(p) + (n << 23));
-}
-// Packed (f32x2) variant of ex2_poly: FADD2/FFMA2 on the FMA pipe.
+// 2^x on the FMA pipe for a pair (offloads the MUFU unit): round-to-nearest
+// split x = n + f, f in [-0.5, 0.5], degree-3 near-minimax polynomial for 2^f
+// (max relative error 1.3e-4, below bf16's half ulp), exponent added as an
+// integer; packed FADD2/FFMA2.
 A2D_DEV float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -126.f);
   x.y = fmaxf(x.y, -126.f);
