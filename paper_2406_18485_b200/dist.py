@@ -185,8 +185,12 @@ class Attn2D:
         d_hp, tok = self.par.d_hp, self.L * self.bd
         self._in_bytes = d_hp * tok * 2 * (self.Hl + 2 * self.Hkl)
         out_bytes = d_hp * tok * (2 * self.Hl + 4 * 2 * self.Hkl)
-        buf = symm.empty(self._in_bytes + out_bytes, dtype=torch.uint8, device=self.device)
-        self._symm = symm.rendezvous(buf, self.hp_group.group_name)
+        try:  # e.g. an HP group spanning nodes cannot map peer memory: keep NCCL
+            buf = symm.empty(self._in_bytes + out_bytes, dtype=torch.uint8, device=self.device)
+            self._symm = symm.rendezvous(buf, self.hp_group.group_name)
+        except RuntimeError:
+            self._symm = None
+            return
         self._symm_buf = buf
         self._peer = [self._symm.get_buffer(r, (buf.numel(),), torch.uint8) for r in range(d_hp)]
         self._xstreams = [torch.cuda.Stream(self.device) for _ in range(d_hp - 1)]
