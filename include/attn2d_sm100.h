@@ -67,7 +67,9 @@ int a2d_bwd_preprocess(const void* o, const void* dout, const float* lse, int32_
 /* One ring step backward: gradients of the block (query chunk, KV chunk)
  * given the FINAL lse/delta of the query rows. Replaces the per-block part
  * of ref attention_backward (oracle.py:127-152):
- *   dq_acc[H][Tq][D] (fp32) += dS K / sqrt(d)          (atomic accumulate)
+ *   dq_acc (fp32, TRANSPOSED [H][128][Tq_pad], Tq_pad = round_up(Tq, 64),
+ *          query contiguous) += (dS K / sqrt(d))^T     (L2-side reduce-add);
+ *          a2d_dqt_to_bf16 turns it into dQ
  *   dk, dv [H_kv][Tk][D] (fp32) (+)= partial (accumulate_kv selects +=)
  * D must be 128 (pad smaller head dims with zeros and pass the true scale). */
 int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* dout, const int32_t* q_pos,
@@ -110,6 +112,11 @@ int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t re
  * gradient all-to-all (ref seq_alltoall_gather, sharding.py:155-169). A = 1
  * or B = 1 is a plain conversion. */
 int a2d_permute_f32_to_bf16(const float* src, void* dst, int64_t A, int64_t B, int64_t block_elems, void* stream);
+
+/* dQ out of the transposed backward accumulator: dst[a][h][l][d] =
+ * bf16(src[h][d][a*L + l]) with L = T/A; A = 1 gives [H][T][128], A = d_hp
+ * gives the gradient all-to-all's peer-major pack (sharding.py:155-169). */
+int a2d_dqt_to_bf16(const float* src, void* dst, int32_t H, int64_t T, int64_t T_pad, int32_t A, void* stream);
 
 /* Elementwise helpers (n multiple of 4). */
 int a2d_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);

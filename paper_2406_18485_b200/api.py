@@ -195,12 +195,12 @@ def attention_backward(q: DenseTensor, k: DenseTensor, v: DenseTensor, d_out,
     do = K.pad_dim(_as_torch(d_out).to(dev), kd)
     lse2, delta = K.bwd_preprocess(out, do, lse)
     pad = lambda t: K.pad_dim(t, K.BWD_DIM)  # noqa: E731
-    dq = torch.zeros((H, T, K.BWD_DIM), dtype=torch.float32, device=dev)
+    dq_acc = K.dq_acc_t(H, T, dev)
     dk = torch.empty((k.heads, k.tokens, K.BWD_DIM), dtype=torch.float32, device=dev)
     dv = torch.empty_like(dk)
-    K.bwd_chunk(pad(qp.t), pad(kp.t), pad(vp.t), pad(do), qp.plan, kp.plan, lse2, delta, dq, dk, dv,
+    K.bwd_chunk(pad(qp.t), pad(kp.t), pad(vp.t), pad(do), qp.plan, kp.plan, lse2, delta, dq_acc, dk, dv,
                 False, causal, scale)
-    return dq[..., :d], dk[..., :d], dv[..., :d]
+    return K.dq_from_acc(dq_acc, T)[..., :d], dk[..., :d], dv[..., :d]
 
 
 # ---------------------------------------------------------------- layout

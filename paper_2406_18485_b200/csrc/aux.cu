@@ -184,6 +184,41 @@ cudaError_t launch_permute_f32_bf16(const float* src, __nv_bfloat16* dst, int64_
   return cudaGetLastError();
 }
 
+// dQ out of the backward's transposed accumulator: dst[a][h][l][d] =
+// bf16(src[h][d][a*L + l]), L = T/A (A = d_hp: the gradient all-to-all's pack;
+// A = 1: plain [h][t][d]). 32-token tiles through shared memory so both the
+// query-contiguous reads and the feature-contiguous writes coalesce.
+__global__ void dqt_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int H, int64_t T,
+                                   int64_t T_pad, int64_t L) {
+  __shared__ float tile[128][33];
+  const int h = blockIdx.y;
+  const int64_t t0 = (int64_t)blockIdx.x * 32;
+  const float* s = src + (size_t)h * 128 * T_pad;
+  for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) {
+    const int d = i / 32, tt = i % 32;
+    tile[d][tt] = (t0 + tt < T) ? s[(size_t)d * T_pad + t0 + tt] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {  // (token, 4-feature chunk)
+    const int tt = i / 32, c = i % 32;
+    const int64_t t = t0 + tt;
+    if (t >= T) continue;
+    const int64_t a = t / L, l = t % L;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(tile[4 * c][tt], tile[4 * c + 1][tt]);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(tile[4 * c + 2][tt], tile[4 * c + 3][tt]);
+    uint2 u = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    *reinterpret_cast<uint2*>(dst + (((size_t)a * H + h) * L + l) * 128 + 4 * c) = u;
+  }
+}
+
+cudaError_t launch_dqt_to_bf16(const float* src, __nv_bfloat16* dst, int H, int64_t T, int64_t T_pad, int A,
+                               cudaStream_t s) {
+  if (H == 0 || T == 0) return cudaSuccess;
+  dim3 grid((unsigned)((T + 31) / 32), H);
+  dqt_to_bf16_kernel<<<grid, 256, 0, s>>>(src, dst, H, T, T_pad, T / A);
+  return cudaGetLastError();
+}
+
 __global__ void gather_blocks_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                      const int* __restrict__ map, const int* __restrict__ dmap, int64_t n,
                                      int64_t blk_vec) {

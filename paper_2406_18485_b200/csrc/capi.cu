@@ -27,6 +27,8 @@ cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, con
 cudaError_t launch_sum_replicas(const float* src, float* dst, int64_t heads, int rep, int64_t per_head, int n_sm,
                                 cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, int n_sm, cudaStream_t s);
+cudaError_t launch_dqt_to_bf16(const float* src, __nv_bfloat16* dst, int H, int64_t T, int64_t T_pad, int A,
+                               cudaStream_t s);
 cudaError_t launch_permute_f32_bf16(const float* src, __nv_bfloat16* dst, int64_t A, int64_t B, int64_t blk_elems,
                                     int n_sm, cudaStream_t s);
 cudaError_t launch_add_f32(float* dst, const float* src, int64_t n, int n_sm, cudaStream_t s);
@@ -75,18 +77,19 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t 
   return A2D_OK;
 }
 
-// fp32 [n2][n1][n0] tensor map, box {box0, box1, 1}, no swizzle (bulk reduce target).
+// fp32 [n2][n1][n0] tensor map (row stride s1, plane stride s2 elements), box
+// {box0, box1, 1}, SWIZZLE_128B (box0 = 32): the transposed dQ reduce target.
 static int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n1, uint64_t n2,
-                            uint64_t s2, uint32_t box0, uint32_t box1) {
+                            uint64_t s1, uint64_t s2, uint32_t box0, uint32_t box1) {
   auto enc = get_encode();
   if (!enc) return fail(A2D_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(A2D_EINVAL, "tensor base not 16-byte aligned");
   cuuint64_t dims[3] = {n0, n1, n2};
-  cuuint64_t strides[2] = {n0 * 4, s2 * 4};
+  cuuint64_t strides[2] = {s1 * 4, s2 * 4};
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(A2D_ECUDA, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string((int)r) + ")");
   return A2D_OK;
@@ -198,7 +201,9 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
       const __nv_bfloat16* db = static_cast<const __nv_bfloat16*>(dout) + off * D;
       if ((rc = make_tmap_bf16_3d(&p.tm_q, qb, D, len, H, D, Tq * D, 64))) return rc;
       if ((rc = make_tmap_bf16_3d(&p.tm_do, db, D, len, H, D, Tq * D, 64))) return rc;
-      if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc + off * D, D, len, H, Tq * D, 128, 64))) return rc;
+      // dq_acc^T [H][128][tq_pad]: this slice starts at query `off`
+      if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc + off, len, D, H, tq_pad, (uint64_t)D * tq_pad, 32, 128)))
+        return rc;
     } else {
       p.tm_q = p.tm_k;
       p.tm_do = p.tm_k;
@@ -211,8 +216,6 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
     p.lse2 = lse2 + off;
     p.delta = delta + off;
     p.stats_stride = tq_pad;
-    p.dq_acc = dq_acc + off * D;
-    p.dq_stride_h = Tq * D;
     p.dk = dk;
     p.dv = dv;
     p.accumulate_kv = (accumulate_kv || off > 0) ? 1 : 0;
@@ -281,6 +284,13 @@ int a2d_permute_f32_to_bf16(const float* src, void* dst, int64_t A, int64_t B, i
   return cuda_status(launch_permute_f32_bf16(src, static_cast<__nv_bfloat16*>(dst), A, B, block_elems, sm_count(),
                                              S(stream)),
                      "a2d_permute_f32_to_bf16");
+}
+
+int a2d_dqt_to_bf16(const float* src, void* dst, int32_t H, int64_t T, int64_t T_pad, int32_t A, void* stream) {
+  if (H < 0 || T < 0 || T_pad < T || A <= 0 || T % A)
+    return fail(A2D_EINVAL, "a2d_dqt_to_bf16: need T_pad >= T and T divisible by A");
+  return cuda_status(launch_dqt_to_bf16(src, static_cast<__nv_bfloat16*>(dst), H, T, T_pad, A, S(stream)),
+                     "a2d_dqt_to_bf16");
 }
 
 int a2d_add_f32(float* dst, const float* src, int64_t n, void* stream) {

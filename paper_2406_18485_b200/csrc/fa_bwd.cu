@@ -23,16 +23,15 @@
 // dS^T also goes through shared memory (SW128) as the MN-major B operand of
 // dQ^T; feeding dK from TMEM saves 16 KB of smem operand reads per iteration
 // (the backward is shared-memory-bandwidth bound).
-// dQ^T is drained TMEM -> smem (fp32 [q][d]) -> TMA bulk tensor reduce-add
-// into dq_acc (the add happens in L2, one 32 KB op per iteration).
+// dQ^T is drained TMEM -> smem -> TMA bulk tensor reduce-add into dq_acc (the
+// add happens in L2). dq_acc is kept TRANSPOSED, [H][128][Tq_pad] (query
+// contiguous), so a drain thread (= one feature d) writes 16-byte runs of 4
+// queries straight from its TMEM row: two SW128 boxes of 32 q x 128 d, 16
+// vector stores per thread instead of 64 scalar ones (+2.7% sustained).
 // Warp roles: 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 two P/dS warpgroups that split
 // every 64-query iteration in halves, 12-15 the dQ^T drain warpgroup.
 #include "sm100.cuh"
 #include "kernels.h"
-
-#ifndef A2D_DQ_RED
-#define A2D_DQ_RED 0  // 1: dQ drained with per-element fp32 reductions instead of smem + TMA reduce
-#endif
 
 namespace a2d {
 
@@ -50,7 +49,7 @@ constexpr int kV = kK + BK * D * 2;              // 32 KB each
 constexpr int kQ = kV + BK * D * 2;              // QST x 16 KB
 constexpr int kDO = kQ + QST * BQ * D * 2;       // QST x 16 KB
 constexpr int kDS = kDO + QST * BQ * D * 2;      // 16 KB  (dS^T, [key][q] SW128)
-constexpr int kDQ = kDS + BK * BQ * 2;           // 32 KB fp32 dQ staging [64 q][128 d]
+constexpr int kDQ = kDS + BK * BQ * 2;           // 32 KB fp32 dQ staging: 2 SW128 boxes [128 d][32 q]
 constexpr int kStats = kDQ + BQ * D * 4;         // QST x (lse2[64], delta[64])
 constexpr int kList = kStats + QST * 2 * BQ * 4; // live query tiles (int)
 constexpr int kEnd = kList + kMaxQTiles * 2;
@@ -266,13 +265,13 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     }
   } else if (warp >= 12) {
     // ------------------------------------------------ dQ^T drain warpgroup
-    // TMEM lane = feature d; 64 query columns -> smem fp32 [q][d] -> one
-    // 32 KB TMA bulk reduce-add into dq_acc per iteration. Runs concurrently
-    // with the P/dS warpgroups, off their critical path.
+    // TMEM lane = feature d; 64 query columns -> two SW128 smem boxes -> TMA
+    // bulk reduce-add into the transposed dq_acc. Runs concurrently with the
+    // P/dS warpgroups, off their critical path.
     const int wq = warp % 4;
     const int d = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    float* dq_stage = reinterpret_cast<float*>(smem + kDQ);  // [64 q][128 d]
+    float* dq_stage = reinterpret_cast<float*>(smem + kDQ);  // 2 boxes [128 d][32 q], SW128
     const bool leader = warp == 12 && lane == 0;
     const float scale = p.scale;
     int it = 0;
@@ -289,36 +288,28 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars.dq_empty[b]);
-#if A2D_DQ_RED
-        // fp32 reductions straight from registers: for each query, the 32
-        // lanes of a warp cover 32 consecutive features (one 128 B line)
-        float* base = p.dq_acc + (size_t)h * p.dq_stride_h + (size_t)(qt * BQ) * D + d;
-        const int rows = min(BQ, p.Tq - qt * BQ);
-        if (rows == BQ) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) atomicAdd(base + (size_t)c * D, __uint_as_float(v0[c]) * scale);
-#pragma unroll
-          for (int c = 0; c < 32; ++c) atomicAdd(base + (size_t)(c + 32) * D, __uint_as_float(v1[c]) * scale);
-        } else {
-          for (int c = 0; c < 32; ++c)
-            if (c < rows) atomicAdd(base + (size_t)c * D, __uint_as_float(v0[c]) * scale);
-          for (int c = 0; c < 32; ++c)
-            if (c + 32 < rows) atomicAdd(base + (size_t)(c + 32) * D, __uint_as_float(v1[c]) * scale);
-        }
-#else
         if (leader) bulk_wait_read0();  // previous reduce finished reading the stage
         named_bar_sync(1, 128);
+        // box b = queries [32b, 32b+32) x all 128 features, SW128: row d, 16-byte
+        // chunk j (queries 4j..4j+3) at position j ^ (d & 7)
+        uint8_t* st = reinterpret_cast<uint8_t*>(dq_stage) + d * 128;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dq_stage[c * D + d] = __uint_as_float(v0[c]) * scale;
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(st + ((c ^ (d & 7)) << 4)) =
+              make_float4(__uint_as_float(v0[4 * c]) * scale, __uint_as_float(v0[4 * c + 1]) * scale,
+                          __uint_as_float(v0[4 * c + 2]) * scale, __uint_as_float(v0[4 * c + 3]) * scale);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dq_stage[(c + 32) * D + d] = __uint_as_float(v1[c]) * scale;
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(st + 16384 + ((c ^ (d & 7)) << 4)) =
+              make_float4(__uint_as_float(v1[4 * c]) * scale, __uint_as_float(v1[4 * c + 1]) * scale,
+                          __uint_as_float(v1[4 * c + 2]) * scale, __uint_as_float(v1[4 * c + 3]) * scale);
         fence_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
-          tma_reduce_add_3d(&p.tm_dq, dq_stage, 0, qt * BQ, h);
+          tma_reduce_add_3d(&p.tm_dq, dq_stage, qt * BQ, 0, h);
+          tma_reduce_add_3d(&p.tm_dq, dq_stage + 4096, qt * BQ + 32, 0, h);
           bulk_commit();
         }
-#endif
       }
     }
     if (leader) bulk_wait0();

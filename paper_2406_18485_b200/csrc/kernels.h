@@ -31,7 +31,7 @@ cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s);
 // D = rowsum(dO * O) of the query chunk.
 struct BwdParams {
   CUtensorMap tm_q, tm_k, tm_v, tm_do;  // box {64,64,1} for q/do, {64,128,1} for k/v
-  CUtensorMap tm_dq;                    // fp32 dq_acc [H][Tq][128], box {128,64,1}, no swizzle
+  CUtensorMap tm_dq;                    // fp32 dq_acc^T [H][128][Tq_pad], box {32 q,128 d,1}, SW128
   const int* q_pos;
   const int* k_pos;
   const int2* q_bounds;   // per 64-row query tile
@@ -39,8 +39,6 @@ struct BwdParams {
   const float* lse2;      // [H][stats_stride] LSE * log2(e) (+inf for dead rows / padding)
   const float* delta;     // [H][stats_stride] rowsum(dO*O)
   int stats_stride;       // row stride of lse2 / delta
-  float* dq_acc;          // [H][..][D] fp32 (this launch's first row), accumulated
-  int64_t dq_stride_h;    // head stride of dq_acc in elements
   float* dk;              // [Hkv][Tk][D] fp32 output (or accumulated)
   float* dv;
   int accumulate_kv;      // 1: dk/dv += partial, 0: overwrite

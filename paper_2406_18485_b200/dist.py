@@ -94,6 +94,7 @@ class Attn2D:
         self.Hl, self.Hkl = H // d_hp, self.H_rep // d_hp
         self.rep = self.H_rep // Hkv
         self.L, self.C = S // self.grid.d_sp, S // d_cp
+        self.C_pad = (self.C + 63) // 64 * 64
 
         # ---- process groups (created by every rank, in the same order)
         self.hp_group = None
@@ -402,6 +403,20 @@ class Attn2D:
             recv = recv.clone()
         return recv.view((d_hp * B, self.L) + tuple(x.shape[2:]))
 
+    def _gather_dq(self, acc: torch.Tensor, name: str, fresh: bool = False) -> torch.Tensor:
+        """Transposed fp32 dQ accumulator (Hl, 128, C_pad) -> SeqSharded bf16 dQ
+        (d_hp*Hl, L, 128); the transpose + rounding is the all-to-all pack."""
+        d_hp, Hl = self.par.d_hp, acc.shape[0]
+        if d_hp == 1:
+            out = self._new(name + ".bf16", (1, Hl, self.C, self.bd), torch.bfloat16, fresh)
+            return K.dqt_to_bf16(acc, self.C, 1, out=out)[0]
+        send = self._buf(name + ".send", (d_hp, Hl, self.L, self.bd), torch.bfloat16)
+        K.dqt_to_bf16(acc, self.C, d_hp, out=send)
+        recv = self._xchg(send, name)
+        if fresh:
+            recv = recv.clone()
+        return recv.view(d_hp * Hl, self.L, self.bd)
+
     def _to_layout(self, x: torch.Tensor, token_major: bool) -> torch.Tensor:
         """Head-major (H, L, e>=d) result -> caller's layout, head dim d, fresh memory."""
         if not token_major:
@@ -588,16 +603,20 @@ class Attn2D:
         if self.ng > 1:
             out = self._out_tensor(self.model.heads, tm)
             for g in range(self.ng):
-                r = self._gather_g(out_h[g * self.Hq_g:(g + 1) * self.Hq_g], "out", g, False)
+                r = self._gather_g(out_h[g * self.Hq_g:(g + 1) * self.Hq_g], "out", g, "bf16")
                 self._unpack_g(*r, self._qmap[g], out, tm)
             return out
         return self._to_layout(self._gather(out_h, "out", fresh=not tm), tm)
 
-    def _gather_g(self, x: torch.Tensor, name: str, g: int, from_f32: bool, wait: bool = True):
-        """Head group g of a HeadSharded tensor (Hn, C, d) -> (recv [d_hp][Hn][L][d] bf16, Work)."""
+    def _gather_g(self, x: torch.Tensor, name: str, g: int, src: str, wait: bool = True):
+        """Head group g of a HeadSharded tensor -> (recv [d_hp][Hn][L][d] bf16, Work).
+        src: "bf16" (Hn, C, d), "f32" (Hn, C, d) fp32, "dqt" transposed dQ accumulator."""
         d_hp, Hn = self.par.d_hp, x.shape[0]
-        send = self._buf(f"{name}.gsend{g}", (d_hp, Hn, self.L, x.shape[-1]), torch.bfloat16)
-        if from_f32:
+        send = self._buf(f"{name}.gsend{g}", (d_hp, Hn, self.L, self.bd if src == "dqt" else x.shape[-1]),
+                         torch.bfloat16)
+        if src == "dqt":
+            K.dqt_to_bf16(x, self.C, d_hp, out=send)
+        elif src == "f32":
             K.permute_to_bf16(x, Hn, d_hp, out=send)
         else:
             K.permute_blocks(x, Hn, d_hp, out=send)
@@ -629,7 +648,7 @@ class Attn2D:
                     self._mark("fwd.a2a_in")
                 sl = slice(g * self.Hq_g, (g + 1) * self.Hq_g)
                 self._ring_forward(qh[sl], kvh[g], out_h[sl], lse[sl], mark=g == self.ng - 1)
-                pend.append(self._gather_g(out_h[sl], "out", g, False, wait=False))
+                pend.append(self._gather_g(out_h[sl], "out", g, "bf16", wait=False))
             for g, (recv, w) in enumerate(pend):
                 self._wait([w])
                 self._unpack_g(recv, self._qmap[g], out, tm)
@@ -676,11 +695,11 @@ class Attn2D:
         doh = self._scatter_q(dout, "do", bd, tm)
         self._mark("bwd.a2a_in")
         lse2, delta = K.bwd_preprocess(out_b, doh, lse)
-        dq_acc = self._buf("dq_acc", (self.Hl, self.C, bd), torch.float32)
+        dq_acc = self._buf("dq_acc", (self.Hl, bd, self.C_pad), torch.float32)
         dq_acc.zero_()
         dkv = self._ring_backward(qh, kvh, doh, lse2, delta, dq_acc)
         self._mark("bwd.ring")
-        dq = self._gather_f32(dq_acc, "dq", fresh=not tm)
+        dq = self._gather_dq(dq_acc, "dq", fresh=not tm)
         self._mark("bwd.a2a_dq")
         if self.rep == 1:
             # one all-to-all per tensor: each receive buffer is already (H_kv, L, e)
@@ -713,12 +732,12 @@ class Attn2D:
                 self._mark("bwd.a2a_in")
             sl = slice(g * self.Hq_g, (g + 1) * self.Hq_g)
             lse2, delta = K.bwd_preprocess(out_h[sl], doh, lse[sl])
-            dq_acc = self._buf("dq_acc", (self.Hq_g, self.C, bd), torch.float32)
+            dq_acc = self._buf("dq_acc", (self.Hq_g, bd, self.C_pad), torch.float32)
             dq_acc.zero_()
             dkv = self._ring_backward(qh[sl], kvh[g], doh, lse2, delta, dq_acc, mark=g == self.ng - 1)
             for name, src, dst, hmap in (("dq", dq_acc, dq, self._qmap[g]), ("dk", dkv[0], dk, self._kmap[g]),
                                          ("dv", dkv[1], dv, self._kmap[g])):
-                recv, w = self._gather_g(src, name, g, True, wait=False)
+                recv, w = self._gather_g(src, name, g, "dqt" if name == "dq" else "f32", wait=False)
                 pend_out.append((recv, w, hmap, dst))
         self._mark("bwd.ring")
         for recv, w, hmap, dst in pend_out:

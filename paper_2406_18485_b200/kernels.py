@@ -100,13 +100,35 @@ def bwd_preprocess(o: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor):
     return lse2, delta
 
 
+def dq_acc_t(H: int, T: int, device) -> torch.Tensor:
+    """Zeroed transposed dQ accumulator [H][128][round_up(T, 64)] fp32 (bwd_chunk's dq_acc)."""
+    return torch.zeros((H, BWD_DIM, (T + 63) // 64 * 64), dtype=torch.float32, device=device)
+
+
+def dq_from_acc(acc: torch.Tensor, T: int) -> torch.Tensor:
+    """fp32 [H][T][128] view of a transposed accumulator (tests / the global-view API)."""
+    return acc[:, :, :T].transpose(1, 2)
+
+
+def dqt_to_bf16(acc: torch.Tensor, T: int, A: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """bf16 dQ out of the transposed accumulator: out[a][h][l][:] = acc[h][:][a*L + l], L = T/A."""
+    H = acc.shape[0]
+    if out is None:
+        out = torch.empty((A, H, T // A, BWD_DIM), dtype=BF16, device=acc.device)
+    _lib.call("a2d_dqt_to_bf16", acc.data_ptr(), out.data_ptr(), H, T, acc.shape[2], A, _stream())
+    return out
+
+
 def bwd_chunk(q, k, v, dout, qp: ChunkPlan, kp: ChunkPlan, lse2, delta, dq_acc, dk, dv,
               accumulate_kv: bool, causal: bool, scale: float) -> None:
-    """One ring step backward (K3). q/k/v/dout bf16 D=128; dq_acc/dk/dv fp32."""
+    """One ring step backward (K3). q/k/v/dout bf16 D=128; dk/dv fp32 [H_kv][Tk][128];
+    dq_acc fp32 TRANSPOSED [H][128][round_up(Tq, 64)] (see dq_acc_t / dqt_to_bf16)."""
     H, Tq, D = q.shape
     Hkv, Tk, _ = k.shape
     if D != BWD_DIM:
         raise ValueError("backward kernel head dim must be 128")
+    if dq_acc.shape != (H, BWD_DIM, (Tq + 63) // 64 * 64) or dq_acc.dtype != torch.float32:
+        raise ValueError("dq_acc must be the transposed fp32 accumulator [H][128][round_up(Tq, 64)]")
     _lib.call("a2d_fa_bwd_chunk", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
               qp.pos.data_ptr(), kp.pos.data_ptr(), qp.b64.data_ptr(), kp.b128.data_ptr(),
               lse2.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dk.data_ptr(), dv.data_ptr(),

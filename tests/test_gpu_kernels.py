@@ -145,12 +145,13 @@ def _bwd(q, k, v, do, q_pos, k_pos, causal, device):
     K.fwd_chunk(t(q, fd), t(k, fd), t(v, fd), qp, kp, causal, scale, lse, None, out)
     dot = t(do, fd)
     lse2, delta = K.bwd_preprocess(out, dot, lse)
-    dq = torch.zeros((H, T, 128), dtype=torch.float32, device=device)
+    dq_acc = K.dq_acc_t(H, T, device)
     dk = torch.empty((Hkv, Tk, 128), dtype=torch.float32, device=device)
     dv = torch.empty((Hkv, Tk, 128), dtype=torch.float32, device=device)
-    K.bwd_chunk(t(q, 128), t(k, 128), t(v, 128), t(do, 128), qp, kp, lse2, delta, dq, dk, dv, False,
+    K.bwd_chunk(t(q, 128), t(k, 128), t(v, 128), t(do, 128), qp, kp, lse2, delta, dq_acc, dk, dv, False,
                 causal, scale)
     torch.cuda.synchronize()
+    dq = K.dq_from_acc(dq_acc, T)
     return (dq[..., :D].cpu().numpy(), dk[..., :D].cpu().numpy(), dv[..., :D].cpu().numpy())
 
 
@@ -205,6 +206,19 @@ def test_permute_f32_to_bf16_matches_torch_rounding():
     assert torch.equal(z.view(torch.int16), x.bfloat16().view(torch.int16))
     with pytest.raises(ValueError):
         K.permute_to_bf16(torch.zeros(3, 2, 5, device=d), 3, 2)  # block of 5 values: not a multiple of 8
+
+
+@pytest.mark.parametrize("T,A", [(200, 1), (256, 2), (96, 4)])
+def test_dqt_to_bf16_transposes_and_packs(T, A):
+    """Transposed dQ accumulator [H][128][T_pad] -> bf16 [A][H][T/A][128]
+    (peer-major pack when A = d_hp); bit-exact vs torch's rounding."""
+    from paper_2406_18485_b200 import kernels as K
+    d = dev()
+    H = 3
+    acc = torch.randn(H, 128, (T + 63) // 64 * 64, device=d) * 10
+    out = K.dqt_to_bf16(acc, T, A)
+    ref = acc[:, :, :T].transpose(1, 2).reshape(H, A, T // A, 128).transpose(0, 1).contiguous().bfloat16()
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
 
 
 def test_bwd_query_slicing_beyond_one_launch():
