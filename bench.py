@@ -132,6 +132,22 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def grid_of(a, world: int):
+    """(d_hp, d_cp, w) of this run: flags, else default_grid(world)."""
+    d_hp, d_cp, w = default_grid(world)
+    d_hp, d_cp = a.d_hp or d_hp, a.d_cp or d_cp
+    w = a.w or (w if (a.d_hp == 0 and a.d_cp == 0) else d_cp)
+    return d_hp, d_cp, w
+
+
+def workload_config(a, world: int) -> dict:
+    """The `config` object both arms print (same workload, same grid)."""
+    d_hp, d_cp, w = grid_of(a, world)
+    return {"workload": f"2D-Attention fwd+bwd MHA H={a.heads} H_kv={a.kv_heads} D={a.dim} S={a.seq} causal",
+            "d_hp": d_hp, "d_cp": d_cp, "w": w, "placement": a.placement, "global_tokens": a.seq,
+            "l2": "inputs > L2 (each q/k/v tensor >= 128 MiB per rank), no flush"}
+
+
 def run_reference(a, rank: int, world: int):
     """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
     if rank != 0:
@@ -153,7 +169,7 @@ def run_reference(a, rank: int, world: int):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": tot / len(times) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"2D-Attention fwd+bwd MHA H={H} D={d} S={S} causal (CPU sample)"},
+        "config": workload_config(a, world),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -201,9 +217,7 @@ def main():
     os.environ.setdefault("MASTER_PORT", "29551")
     if not dist.is_initialized():
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
-    d_hp, d_cp, w = default_grid(world)
-    d_hp, d_cp = a.d_hp or d_hp, a.d_cp or d_cp
-    w = a.w or (w if (a.d_hp == 0 and a.d_cp == 0) else d_cp)
+    d_hp, d_cp, w = grid_of(a, world)
     S, H, Hkv, d = a.seq, a.heads, a.kv_heads, a.dim
     model = ModelConfig(seq_len=S, heads=H, kv_heads=Hkv, hidden=H * d)
     par = ParallelConfig(d_hp=d_hp, d_cp=d_cp, inner_ring=w, placement=Placement(a.placement))
@@ -387,9 +401,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random bf16 q/k/v/dO)",
-            "config": {"workload": f"2D-Attention fwd+bwd MHA H={H} H_kv={Hkv} D={d} S={S} causal",
-                       "d_hp": d_hp, "d_cp": d_cp, "w": w, "placement": a.placement,
-                       "global_tokens": S, "l2": "inputs > L2 (each q/k/v tensor >= 128 MiB per rank), no flush"},
+            "config": workload_config(a, world),
             "tflops_per_gpu": per_gpu, "mfu": per_gpu / pk["bf16_tflops"],
             "mfu_sustained": per_gpu / pk["bf16_tflops_sustained"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
