@@ -499,7 +499,11 @@ class Attn2D:
             return dkv
         part = self._buf("bwd.part", shape, torch.float32)
         acc = [self._buf(f"bwd.acc{i}", shape, torch.float32) for i in range(2)]
-        home = self._buf("bwd.dkv_home", shape, torch.float32)
+        # The home rank adds nothing after the last hop and rounds to bf16 anyway:
+        # without GQA replicas (summed in fp32 after the gather) the last hop
+        # carries bf16 — bit-identical, half the bytes of the exposed hop.
+        home_bf16 = self.rep == 1
+        home = self._buf("bwd.dkv_home", shape, torch.bfloat16 if home_bf16 else torch.float32)
         inner = [self._buf(f"kvb.in{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
         outer = [self._buf(f"kvb.out{i}", kv_own.shape, kv_own.dtype) for i in range(2)]
         cur, first = kv_own, kv_own
@@ -530,7 +534,10 @@ class Attn2D:
                 to, frm = self.inner_to, self.inner_from
             else:
                 to, frm = self.diag_to, self.diag_from
-            w_dkv = self._p2p(self.ring_dkv, acc[s % 2], to, dst, frm)
+            src = acc[s % 2]
+            if last and home_bf16:
+                src = K.to_bf16(src, self._buf("bwd.dkv_send", shape, torch.bfloat16))
+            w_dkv = self._p2p(self.ring_dkv, src, to, dst, frm)
             if t + 1 < w:
                 self._wait(w_in)
                 cur = nxt_inner
@@ -702,8 +709,10 @@ class Attn2D:
         dq = self._gather_dq(dq_acc, "dq", fresh=not tm)
         self._mark("bwd.a2a_dq")
         if self.rep == 1:
-            # one all-to-all per tensor: each receive buffer is already (H_kv, L, e)
-            dk, dv = self._gather_f32(dkv[0], "dk", fresh=not tm), self._gather_f32(dkv[1], "dv", fresh=not tm)
+            # one all-to-all per tensor: each receive buffer is already (H_kv, L, e);
+            # dkv is bf16 when it arrived by the ring's last hop, fp32 straight from the kernel
+            gather = self._gather if dkv.dtype == torch.bfloat16 else self._gather_f32
+            dk, dv = gather(dkv[0], "dk", fresh=not tm), gather(dkv[1], "dv", fresh=not tm)
         else:  # GQA replicas: gather fp32, sum the Ĥ/H_kv copies, then round once
             dk = K.to_bf16(K.sum_replicas(self._gather(dkv[0], "dk32"), self.rep))
             dv = K.to_bf16(K.sum_replicas(self._gather(dkv[1], "dv32"), self.rep))
@@ -737,7 +746,8 @@ class Attn2D:
             dkv = self._ring_backward(qh[sl], kvh[g], doh, lse2, delta, dq_acc, mark=g == self.ng - 1)
             for name, src, dst, hmap in (("dq", dq_acc, dq, self._qmap[g]), ("dk", dkv[0], dk, self._kmap[g]),
                                          ("dv", dkv[1], dv, self._kmap[g])):
-                recv, w = self._gather_g(src, name, g, "dqt" if name == "dq" else "f32", wait=False)
+                kind = "dqt" if name == "dq" else ("bf16" if src.dtype == torch.bfloat16 else "f32")
+                recv, w = self._gather_g(src, name, g, kind, wait=False)
                 pend_out.append((recv, w, hmap, dst))
         self._mark("bwd.ring")
         for recv, w, hmap, dst in pend_out:

@@ -30,8 +30,21 @@ CASES = [
     (1, 4, 2, "head_first", 4, 4, 2048, 128),
     (1, 4, 4, "context_first", 4, 1, 2048, 128),
     (4, 1, 1, "head_first", 8, 2, 1024, 128),  # GQA replication: H_kv=2 < d_hp=4
+    (2, 2, 2, "head_first", 4, 1, 1024, 128),  # replication AND a ring: the fp32 dK/dV home hop
     (2, 2, 2, "context_first", 8, 8, 1024, 64),
 ]
+
+
+def test_dist_non_causal(tmp_path):
+    """Full (non-causal) attention through the 2x2 runtime."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    res = _run(4, ["--d-hp", "2", "--d-cp", "2", "--w", "1", "--placement", "head_first", "--heads", "8",
+                   "--kv-heads", "4", "--seq", "1024", "--dim", "128", "--causal", "0"], tmp_path)
+    for name in ("O", "dQ", "dK", "dV"):
+        ma, rl, rng = res[name]
+        assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
+            f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
 
 
 def _run(nproc, args, tmp_path, env=None):
