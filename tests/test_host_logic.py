@@ -227,3 +227,38 @@ def test_gloo_ring_exchange(d_cp, w):
     for rank, got, want, acc in res:
         assert got == want, (rank, got, want)
         assert acc == [rank, d_cp, True], (rank, acc)  # home, visited by every CP rank, in order
+
+
+@pytest.mark.parametrize("d_hp,Hl,Hkl,ng", [(2, 16, 16, 1), (4, 8, 2, 1), (2, 16, 16, 4), (8, 4, 4, 2), (2, 4, 1, 1)])
+def test_symm_exchange_layout_fits_and_is_disjoint(d_hp, Hl, Hkl, ng):
+    """Byte layout of the symmetric-memory exchange buffer (dist.Attn2D._xoff):
+    every exchange fits inside the allocation, and exchanges that can be in
+    flight together (all groups of one phase; q with kv; dq with dk and dv;
+    the fp32 GQA gathers) never overlap."""
+    from types import SimpleNamespace
+    from paper_2406_18485_b200.dist import Attn2D
+    L, bd = 1024, 128
+    op = SimpleNamespace(par=SimpleNamespace(d_hp=d_hp), L=L, bd=bd, Hl=Hl, Hkl=Hkl, ng=ng,
+                         Hq_g=Hl // ng, Hk_g=Hkl // ng)
+    tok = L * bd
+    op._in_bytes = d_hp * tok * 2 * (Hl + 2 * Hkl)
+    total = op._in_bytes + d_hp * tok * (2 * Hl + 4 * 2 * Hkl)
+    off = lambda name, g=0: Attn2D._xoff(op, name, g)  # noqa: E731
+    q_b, kv_b, k_b = d_hp * tok * 2 * op.Hq_g, d_hp * tok * 2 * 2 * op.Hk_g, d_hp * tok * 2 * op.Hk_g
+    phases = [
+        [(off("q", g), q_b) for g in range(ng)] + [(off("kv", g), kv_b) for g in range(ng)],   # fwd in
+        [(off("do", g), q_b) for g in range(ng)],                                              # bwd in
+        [(off("out", g), q_b) for g in range(ng)],                                             # fwd out
+        [(off(n, g), b) for g in range(ng) for n, b in (("dq", q_b), ("dk", k_b), ("dv", k_b))],  # bwd out
+    ]
+    if ng == 1:
+        phases.append([(off("dq"), q_b), (off("dk32"), 2 * k_b), (off("dv32"), 2 * k_b)])  # GQA replicas
+    for spans in phases:
+        for o, b in spans:
+            assert 0 <= o and o + b <= total
+        spans = sorted(spans)
+        for (o1, b1), (o2, _) in zip(spans, spans[1:]):
+            assert o1 + b1 <= o2, spans
+    # scatters use the IN region, gathers the OUT region
+    assert all(o + b <= op._in_bytes for o, b in phases[0] + phases[1])
+    assert all(o >= op._in_bytes for o, _ in phases[2] + phases[3])
