@@ -29,8 +29,8 @@ class B200Calibration:
     """Measured on B200 (round 1): tools/kbench.py, bench.py sweeps, tools/trace.py
     phase traces (profiles/r01_trace_*.json), guide peaks."""
 
-    fwd_tflops: float = 1100.0     # forward chunk kernel in a full step (kbench alone: 1152 at S=128K)
-    bwd_tflops: float = 940.0      # backward chunk kernel in a full step (kbench alone: 980)
+    fwd_tflops: float = 1180.0     # forward chunk kernel in a full step (final round-1 build)
+    bwd_tflops: float = 1040.0     # backward chunk kernel in a full step (final round-1 build)
     short_chunk_tokens: float = 500.0   # kernel efficiency ~ C / (C + this) for small chunks
     a2a_gbs: float = 620.0         # NCCL all_to_all_single: time ~ whole buffer / this (traces, d_hp = 2 and 4)
     ce_gbs: float = 770.0          # copy-engine write into a peer's symmetric buffer (tools/probes/peer_probe.py)
@@ -46,6 +46,11 @@ class B200Calibration:
 
 def calibration() -> B200Calibration:
     return B200Calibration()
+
+
+# The earlier round-1 build that produced profiles/r01_sweep_*.jsonl (NCCL
+# all-to-all, backward before the transposed-dQ drain).
+EARLY_ROUND1 = B200Calibration(fwd_tflops=1100.0, bwd_tflops=940.0, transport="nccl")
 
 
 def _eff(c: B200Calibration, tokens: int) -> float:
@@ -146,7 +151,7 @@ def plan(model: ModelConfig, n_gpus: int, cal: B200Calibration | None = None, ca
 def check_against_sweep(path: str, cal: B200Calibration | None = None) -> dict:
     """Compare predictions with a measured sweep (tools/sweep.py JSONL; the
     round-1 sweeps ran the NCCL transport)."""
-    cal = cal or B200Calibration(transport="nccl")
+    cal = cal or calibration()
     errs, pairs = [], []
     for line in open(path):
         r = json.loads(line)

@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
     ap.add_argument("--timeout", type=int, default=600)
+    ap.add_argument("--placements", nargs="+", default=["head_first", "context_first"])
     a = ap.parse_args()
     model = ModelConfig(seq_len=a.seq, heads=a.heads, kv_heads=a.kv_heads, hidden=a.heads * 128)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
@@ -48,6 +49,8 @@ def main():
     with open(a.out, "a") as f:
         for n in a.gpus:
             for d_hp, d_cp, w, pl in configs(n, model):
+                if pl not in a.placements:
+                    continue
                 port += 1
                 cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                        "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
