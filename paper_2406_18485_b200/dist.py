@@ -1,19 +1,23 @@
-"""SPMD 2D-Attention runtime: one process per GPU, NCCL over NVLink.
+"""SPMD 2D-Attention runtime: one process per GPU over NVLink.
 
 Alg. 1 of the paper (ref ``ring.py:82-119``) executed for real:
 
-  SeqSharded q/k/v (H, L, d) per rank
+  SeqSharded q/k/v (H, L, d) per rank (head-major, or token-major views of a
+  fused QKV projection)
     -> pack (128-bit gather kernel; GQA replication by addressing)
-    -> NCCL all-to-all inside the HP group (d_hp ranks sharing a cp_index)
+    -> all-to-all inside the HP group (d_hp ranks sharing a cp_index): by
+       default copy-engine writes straight into the peers' torch
+       symmetric-memory buffers + a device barrier (``_xchg``); NCCL
+       ``all_to_all_single`` with A2D_TRANSPORT=nccl
     -> unpack (128-bit permute kernel) = HeadSharded (H/d_hp, C, d)
     -> Double-Ring attention inside the CP group (d_cp ranks sharing an
        hp_index): KV chunks rotate over an inner ring of size w and an outer
-       ring of d_cp/w, as NCCL send/recv on two separate communicators so an
+       ring of d_cp/w, as NCCL send/recv on separate communicators so an
        outer hop (issued at the start of an outer step) overlaps the w inner
        hops and the attention kernels (Alg. 2);
        each step folds its block into an fp32 accumulator inside the
        attention kernel's epilogue
-    -> pack + NCCL all-to-all back -> SeqSharded output (H, L, d)
+    -> pack + all-to-all back -> SeqSharded output (H, L, d)
 
 Backward (not in the reference; designed here and checked
 against the global oracle): KV chunks rotate again along the same schedule;
@@ -21,10 +25,12 @@ a travelling fp32 dK/dV accumulator follows each chunk one step behind and
 is added to (K4 kernel) by every rank that consumes the chunk. The
 accumulator's hop is (r, p) -> (r, p+1) inside an outer step and the
 "diagonal" (r, p) -> (r+1, p+1) across outer steps; the same diagonal hop
-after the last step brings every accumulator home to its owner.
+after the last step brings every accumulator home to its owner (in bf16
+when nothing is added at home). dQ accumulates in a transposed fp32 buffer
+that the gradient all-to-all's pack turns into bf16.
 
-All comm runs on NCCL's internal streams; ``Work.wait()`` only makes the
-compute stream wait (no host sync).
+Communication never blocks the host: ``Work.wait()`` / stream events only
+make the compute stream wait.
 """
 
 from __future__ import annotations
