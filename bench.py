@@ -123,6 +123,25 @@ def cpu_sample(rows: int, S: int, d: int, seed: int = 0):
     return dt, flops
 
 
+class all_blas_threads:
+    """Use every core this process may run on for the numpy/BLAS CPU legs
+    (torchrun sets OMP_NUM_THREADS=1, which would silently cap them at one)."""
+
+    def __enter__(self):
+        try:
+            from threadpoolctl import threadpool_limits
+            n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+            self._ctl = threadpool_limits(limits=n, user_api="blas")
+        except Exception:
+            self._ctl = None
+        return self
+
+    def __exit__(self, *exc):
+        if self._ctl is not None:
+            self._ctl.restore_original_limits()
+        return False
+
+
 def cpu_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -154,13 +173,15 @@ def run_reference(a, rank: int, world: int):
         return 0
     S, H, d = a.seq, a.heads, a.dim
     rows = a.cpu_rows
-    for _ in range(a.warmup if a.warmup < 1 else 1):
-        cpu_sample(64, S, d)
     times, flops = [], 0.0
-    for _ in range(a.steps):
-        dt, fl = cpu_sample(rows, S, d)
-        times.append(dt)
-        flops = fl
+    with all_blas_threads():
+        for _ in range(a.warmup if a.warmup < 1 else 1):
+            cpu_sample(64, S, d)
+        for _ in range(a.steps):
+            dt, fl = cpu_sample(rows, S, d)
+            times.append(dt)
+            flops = fl
+        cores = cpu_cores()
     tot = sum(times)
     val = flops * len(times) / tot / 1e12
     sample = f"1 head x last {rows} query rows x {S} keys, d={d}, causal fwd+bwd, f64 numpy (oracle port)"
@@ -170,7 +191,7 @@ def run_reference(a, rank: int, world: int):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": workload_config(a, world),
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
@@ -393,8 +414,10 @@ def main():
                 "fwd_kernel": {"achieved": fwd_achieved, "share_of_step": fwd_ms / t_ms if t_ms else None}}
         cpu = None
         if world == 1 and not a.no_cpu:
-            dt, fl = cpu_sample(a.cpu_rows, S, d)
-            cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+            with all_blas_threads():
+                dt, fl = cpu_sample(a.cpu_rows, S, d)
+                cores = cpu_cores()
+            cpu = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "port",
                    "sample": f"1 head x last {a.cpu_rows} query rows x {S} keys, d={d}, causal fwd+bwd, "
                              f"f64 numpy oracle port, {dt:.2f} s"}
         line = {
