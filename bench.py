@@ -18,6 +18,14 @@ region. Rank 0 prints one JSON line.
 
 from __future__ import annotations
 
+import os as _os
+import sys as _sys
+
+if "reference" in _sys.argv:  # CPU arm: undo torchrun's OMP_NUM_THREADS=1 before numpy loads its BLAS
+    _n = str(len(_os.sched_getaffinity(0)) if hasattr(_os, "sched_getaffinity") else (_os.cpu_count() or 1))
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        _os.environ[_v] = _n
+
 import argparse
 import json
 import math
