@@ -284,7 +284,7 @@ def main():
     dist.barrier()
     clk = clocks.stop()
     t_ms = e0.elapsed_time(e1)
-    launches = _lib.LOG.count // a.steps
+    launches = _lib.LOG.count            # our kernels launched in the timed region (all K steps)
     kern = {"a2d_fa_bwd_chunk": [0.0, 0], "a2d_fa_fwd_chunk": [0.0, 0]}
     for name, s0, s1 in _lib.LOG.events:
         kern[name][0] += s0.elapsed_time(s1)
@@ -436,6 +436,7 @@ def main():
             "tflops_per_gpu": per_gpu, "mfu": per_gpu / pk["bf16_tflops"],
             "mfu_sustained": per_gpu / pk["bf16_tflops_sustained"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "gpu_launches_per_step": launches / a.steps,
             "clocks": clk, "exposed_comm": exposed,
         }
         print(json.dumps(line))
