@@ -122,6 +122,30 @@ int a2d_dqt_to_bf16(const float* src, void* dst, int32_t H, int64_t T, int64_t T
 int a2d_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 int a2d_add_f32(float* dst, const float* src, int64_t n, void* stream);
 
+/* ---- Native SPMD runtime (SURVEY §8b "C-ABI to export"): the whole 2D
+ * attention layer of one rank, NCCL inside the library. One process per GPU;
+ * rank r of a world of d_hp*d_cp ranks, placement 0 = head-first
+ * (rank = hp + d_hp*cp), 1 = context-first (rank = cp + d_cp*hp), as the
+ * reference's RankGrid (config.py:155-163). Tensors are this rank's
+ * SeqSharded chunks, head-major bf16 device arrays: q/out/dout/dq [H][L][d],
+ * k/v/dk/dv [H_kv][L][d], L = S/(d_hp*d_cp), tokens in zig-zag order (ref
+ * shard_sequence, sharding.py:56-79). Head dim 128. One forward in flight per
+ * context; its state is kept for the next a2d_bwd (with d_hp = 1 the caller's
+ * q must stay valid until then). */
+/* Rank 0 creates the NCCL id (128 bytes) and shares it with the other ranks. */
+int a2d_nccl_unique_id(void* out, int64_t out_bytes);
+/* Collective over all `world` ranks: communicators (HP all-to-all group; inner,
+ * outer and dK/dV ring groups), ring schedule (ring.py:41-61), positions,
+ * buffers. Replaces run_2d_attention's setup (ring.py:82-107). */
+int a2d_ctx_create(const void* nccl_id, int32_t rank, int32_t world, int32_t d_hp, int32_t d_cp, int32_t w,
+                   int32_t placement, int32_t H, int32_t H_kv, int32_t d, int64_t S, int32_t causal, void** ctx);
+/* Forward of the layer (ref run_2d_attention, ring.py:82-119): out = this
+ * rank's SeqSharded output. Collective; stream-ordered on `stream`. */
+int a2d_fwd(void* ctx, const void* q, const void* k, const void* v, void* out, void* stream);
+/* Backward of the last a2d_fwd: dq, dk, dv SeqSharded bf16. Collective. */
+int a2d_bwd(void* ctx, const void* dout, void* dq, void* dk, void* dv, void* stream);
+int a2d_ctx_destroy(void* ctx);
+
 /* UMMA plumbing self-test (one CTA, 128x128x128 bf16 GEMMs in four operand
  * layouts); c is fp32 [4][128][128]. Used by the parity tests. */
 int a2d_selftest_umma(const void* a, const void* b, const void* v, const void* at, float* c, void* stream);

@@ -34,6 +34,12 @@ SIGNATURES = {
     "a2d_dqt_to_bf16": [_vp, _vp, _c_i32, _c_i64, _c_i64, _c_i32, _vp],
     "a2d_add_f32": [_vp, _vp, _c_i64, _vp],
     "a2d_selftest_umma": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "a2d_nccl_unique_id": [_vp, _c_i64],
+    "a2d_ctx_create": [_vp, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_i32,
+                       _vp],
+    "a2d_fwd": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "a2d_bwd": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "a2d_ctx_destroy": [_vp],
 }
 
 _lib = None

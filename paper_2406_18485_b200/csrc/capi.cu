@@ -108,6 +108,9 @@ static int sm_count() {
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// for runtime.cu: report through the same thread-local a2d_last_error()
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+
 }  // namespace a2d
 
 using namespace a2d;

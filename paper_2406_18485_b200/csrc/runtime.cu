@@ -1,0 +1,474 @@
+// Native SPMD 2D-Attention runtime behind the context C ABI:
+//   a2d_nccl_unique_id / a2d_ctx_create / a2d_fwd / a2d_bwd / a2d_ctx_destroy.
+//
+// The same algorithm as the Python runtime dist.Attn2D with its NCCL
+// transport (ref run_2d_attention, ring.py:82-119, plus the distributed
+// backward designed there): one process per GPU; head-parallel all-to-all as
+// grouped ncclSend/ncclRecv inside the HP communicator; Double-Ring KV
+// rotation (inner ring w, outer ring d_cp/w) as point-to-point hops on three
+// communicators (inner / outer / dK-dV accumulator), each on its own side
+// stream and ordered against the compute stream with events, so a hop
+// overlaps the attention kernel beside it. The compute is the library's own
+// chunk kernels (a2d_fa_fwd_chunk, a2d_fa_bwd_chunk, packs, conversions).
+// Scope: head dim 128, head-major [H][L][d] SeqSharded tensors in zig-zag
+// token order (layout.seq_positions); one forward in flight per context (its
+// state is kept for the matching a2d_bwd, and with d_hp = 1 the caller's q
+// must stay valid until then).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/attn2d_sm100.h"
+
+namespace a2d {
+int set_error(int code, const std::string& msg);
+}
+
+namespace {
+
+using a2d::set_error;
+
+struct Step {
+  int source, inner, outer;
+};
+
+struct Ctx {
+  int rank = 0, world = 1, d_hp = 1, d_cp = 1, w = 1, placement = 0, H = 0, Hkv = 0, d = 128, causal = 1;
+  int64_t S = 0, L = 0, C = 0, C_pad = 0;
+  int hp = 0, cp = 0, Hl = 0, Hkl = 0, H_rep = 0, rep = 1, n_outer = 1;
+  float scale = 0.f;
+  ncclComm_t world_comm = nullptr, hp_comm = nullptr, c_inner = nullptr, c_outer = nullptr, c_dkv = nullptr;
+  cudaStream_t s_inner = nullptr, s_outer = nullptr, s_dkv = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_inner = nullptr, ev_outer = nullptr, ev_dkv = nullptr;
+  std::vector<Step> steps;
+  int inner_to = 0, inner_from = 0, outer_to = 0, outer_from = 0, diag_to = 0, diag_from = 0;
+  std::vector<int32_t*> pos, b128, b64;  // per CP chunk j (device)
+  int32_t *smap = nullptr, *dmap_k = nullptr, *dmap_v = nullptr;
+  std::vector<void*> allocs;
+  // buffers
+  uint16_t *kv_send = nullptr, *q_recv = nullptr, *kv_recv = nullptr, *qh_own = nullptr, *kvh = nullptr;
+  uint16_t *out_h = nullptr, *out_send = nullptr, *doh = nullptr, *g_send = nullptr, *dkv_send = nullptr;
+  uint16_t* ring[4] = {nullptr, nullptr, nullptr, nullptr};  // inner0, inner1, outer0, outer1
+  float *lse = nullptr, *acc = nullptr, *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr;
+  float *dkv = nullptr, *part = nullptr, *dacc[2] = {nullptr, nullptr}, *g32_send = nullptr, *g32_recv = nullptr;
+  float* g32_sum = nullptr;
+  void* dkv_home = nullptr;
+  const uint16_t* qh = nullptr;   // qh_own, or the caller's q when d_hp == 1
+  const uint16_t* dO = nullptr;   // doh, or the caller's dout when d_hp == 1
+  bool have_state = false;
+};
+
+#define NCCL_TRY(x)                                                                                  \
+  do {                                                                                               \
+    ncclResult_t r_ = (x);                                                                           \
+    if (r_ != ncclSuccess) return set_error(A2D_ECUDA, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+#define CUDA_TRY(x)                                                                                  \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess) return set_error(A2D_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define A2D_TRY(x)      \
+  do {                  \
+    int rc_ = (x);      \
+    if (rc_) return rc_; \
+  } while (0)
+
+template <class T>
+int dalloc(Ctx& c, T** p, size_t n) {
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)));
+  c.allocs.push_back(*p);
+  return A2D_OK;
+}
+
+int src_of(int j, int o, int t, int w, int n) {  // ring.py:53-59
+  const int ring = j / w, pos = j % w;
+  return ((ring - o) % n + n) % n * w + ((pos - t) % w + w) % w;
+}
+
+// grouped send/recv of bytes_per_peer to/from every member of the HP group
+int a2a(Ctx& c, const void* send, void* recv, size_t bytes_per_peer, cudaStream_t s) {
+  NCCL_TRY(ncclGroupStart());
+  for (int p = 0; p < c.d_hp; ++p) {
+    NCCL_TRY(ncclSend(static_cast<const char*>(send) + p * bytes_per_peer, bytes_per_peer, ncclUint8, p, c.hp_comm, s));
+    NCCL_TRY(ncclRecv(static_cast<char*>(recv) + p * bytes_per_peer, bytes_per_peer, ncclUint8, p, c.hp_comm, s));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return A2D_OK;
+}
+
+// one ring hop on a side stream, ordered after everything enqueued on `main` so far
+int hop(Ctx& c, ncclComm_t comm, cudaStream_t side, cudaStream_t main, const void* send, int to, void* recv, int from,
+        size_t bytes, cudaEvent_t done) {
+  CUDA_TRY(cudaEventRecord(c.ev_ready, main));
+  CUDA_TRY(cudaStreamWaitEvent(side, c.ev_ready, 0));
+  NCCL_TRY(ncclGroupStart());
+  NCCL_TRY(ncclSend(send, bytes, ncclUint8, to, comm, side));
+  NCCL_TRY(ncclRecv(recv, bytes, ncclUint8, from, comm, side));
+  NCCL_TRY(ncclGroupEnd());
+  CUDA_TRY(cudaEventRecord(done, side));
+  return A2D_OK;
+}
+
+// zig-zag positions of CP chunk j (layout.cp_positions)
+std::vector<int32_t> cp_positions(int64_t S, int d_cp, int j) {
+  const int64_t sigma = S / (2 * d_cp), C = S / d_cp;
+  std::vector<int32_t> out(C);
+  for (int64_t u = 0; u < C; ++u) {
+    const int64_t slot = j * C + u;
+    const int64_t jj = slot / (2 * sigma), uu = slot % (2 * sigma);
+    const int64_t stripe = uu < sigma ? jj : 2 * d_cp - 1 - jj;
+    out[u] = (int32_t)(stripe * sigma + uu % sigma);
+  }
+  return out;
+}
+
+int destroy(Ctx* c) {
+  if (!c) return A2D_OK;
+  cudaDeviceSynchronize();
+  for (ncclComm_t* m : {&c->c_dkv, &c->c_outer, &c->c_inner, &c->hp_comm, &c->world_comm})
+    if (*m) ncclCommDestroy(*m);
+  for (cudaStream_t s : {c->s_inner, c->s_outer, c->s_dkv})
+    if (s) cudaStreamDestroy(s);
+  for (cudaEvent_t e : {c->ev_ready, c->ev_inner, c->ev_outer, c->ev_dkv})
+    if (e) cudaEventDestroy(e);
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+  return A2D_OK;
+}
+
+// dst = this rank's SeqSharded tensor; src HeadSharded (B heads, C tokens, 128):
+// pack [peer][B][L][128] then all-to-all (d_hp = 1: plain copy / conversion)
+int gather_bf16(Ctx& c, const uint16_t* src, int B, uint16_t* dst, cudaStream_t s) {
+  const size_t chunk = (size_t)B * c.L * 128 * 2;
+  if (c.d_hp == 1) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, chunk, cudaMemcpyDeviceToDevice, s));
+    return A2D_OK;
+  }
+  A2D_TRY(a2d_permute_blocks(src, c.g_send, B, c.d_hp, (int64_t)c.L * 128 * 2, s));
+  return a2a(c, c.g_send, dst, chunk, s);
+}
+
+int gather_f32_to_bf16(Ctx& c, const float* src, int B, uint16_t* dst, cudaStream_t s) {
+  if (c.d_hp == 1) return a2d_permute_f32_to_bf16(src, dst, 1, 1, (int64_t)B * c.C * 128, s);
+  A2D_TRY(a2d_permute_f32_to_bf16(src, c.g_send, B, c.d_hp, (int64_t)c.L * 128, s));
+  return a2a(c, c.g_send, dst, (size_t)B * c.L * 128 * 2, s);
+}
+
+int ring_forward(Ctx& c, cudaStream_t s) {
+  const size_t kv_elems = (size_t)2 * c.Hkl * c.C * 128, kv_bytes = kv_elems * 2, half = kv_elems / 2;
+  const int64_t q_rows = (int64_t)c.C;
+  if (c.d_cp == 1)
+    return a2d_fa_fwd_chunk(c.qh, c.kvh, c.kvh + half, c.pos[c.cp], c.pos[c.cp], c.b128[c.cp], c.b128[c.cp], c.Hl, c.Hkl,
+                            q_rows, q_rows, 128, c.causal, c.scale, 0, c.lse, nullptr, c.out_h, s);
+  const uint16_t *cur = c.kvh, *first = c.kvh;
+  uint16_t* nxt_inner = nullptr;
+  uint16_t* nxt_outer = nullptr;
+  int n_out = 0;
+  for (int st = 0; st < c.d_cp; ++st) {
+    const Step step = c.steps[st];
+    const int t = step.inner, o = step.outer;
+    const bool last = st == c.d_cp - 1;
+    if (t == 0 && o + 1 < c.n_outer) {
+      nxt_outer = c.ring[2 + n_out % 2];
+      ++n_out;
+      A2D_TRY(hop(c, c.c_outer, c.s_outer, s, first, c.outer_to, nxt_outer, c.outer_from, kv_bytes, c.ev_outer));
+    }
+    if (t + 1 < c.w) {
+      nxt_inner = c.ring[(t + 1) % 2];
+      A2D_TRY(hop(c, c.c_inner, c.s_inner, s, cur, c.inner_to, nxt_inner, c.inner_from, kv_bytes, c.ev_inner));
+    }
+    A2D_TRY(a2d_fa_fwd_chunk(c.qh, cur, cur + half, c.pos[c.cp], c.pos[step.source], c.b128[c.cp],
+                             c.b128[step.source], c.Hl, c.Hkl, q_rows, q_rows, 128, c.causal, c.scale, st > 0 ? 1 : 0,
+                             c.lse, c.acc, last ? c.out_h : nullptr, s));
+    if (t + 1 < c.w) {
+      CUDA_TRY(cudaStreamWaitEvent(s, c.ev_inner, 0));
+      cur = nxt_inner;
+    } else if (!last) {
+      CUDA_TRY(cudaStreamWaitEvent(s, c.ev_outer, 0));
+      cur = first = nxt_outer;
+    }
+  }
+  return A2D_OK;
+}
+
+// returns the home dK/dV buffer ([2][Hkl][C][128]) and whether it is bf16
+int ring_backward(Ctx& c, cudaStream_t s, const void** home, bool* home_bf16) {
+  const size_t kv_elems = (size_t)2 * c.Hkl * c.C * 128, kv_bytes = kv_elems * 2, half = kv_elems / 2;
+  const int64_t T = (int64_t)c.C;
+  const uint16_t* kv_own = c.kvh;
+  if (c.d_cp == 1) {
+    A2D_TRY(a2d_fa_bwd_chunk(c.qh, kv_own, kv_own + half, c.dO, c.pos[c.cp], c.pos[c.cp], c.b64[c.cp], c.b128[c.cp],
+                             c.lse2, c.delta, c.dq_acc, c.dkv, c.dkv + half, 0, c.Hl, c.Hkl, T, T, 128, c.causal,
+                             c.scale, s));
+    *home = c.dkv;
+    *home_bf16 = false;
+    return A2D_OK;
+  }
+  const bool hb = c.rep == 1;  // home adds nothing: the last hop may carry bf16 (bit-identical)
+  const uint16_t *cur = kv_own, *first = kv_own;
+  uint16_t *nxt_inner = nullptr, *nxt_outer = nullptr;
+  int n_out = 0;
+  for (int st = 0; st < c.d_cp; ++st) {
+    const Step step = c.steps[st];
+    const int t = step.inner, o = step.outer;
+    const bool last = st == c.d_cp - 1;
+    if (t == 0 && o + 1 < c.n_outer) {
+      nxt_outer = c.ring[2 + n_out % 2];
+      ++n_out;
+      A2D_TRY(hop(c, c.c_outer, c.s_outer, s, first, c.outer_to, nxt_outer, c.outer_from, kv_bytes, c.ev_outer));
+    }
+    if (t + 1 < c.w) {
+      nxt_inner = c.ring[(t + 1) % 2];
+      A2D_TRY(hop(c, c.c_inner, c.s_inner, s, cur, c.inner_to, nxt_inner, c.inner_from, kv_bytes, c.ev_inner));
+    }
+    float* tgt = st == 0 ? c.dacc[0] : c.part;
+    A2D_TRY(a2d_fa_bwd_chunk(c.qh, cur, cur + half, c.dO, c.pos[c.cp], c.pos[step.source], c.b64[c.cp],
+                             c.b128[step.source], c.lse2, c.delta, c.dq_acc, tgt, tgt + half, 0, c.Hl, c.Hkl, T, T, 128,
+                             c.causal, c.scale, s));
+    if (st > 0) {  // the travelling accumulator of this chunk arrived in dacc[st % 2]
+      CUDA_TRY(cudaStreamWaitEvent(s, c.ev_dkv, 0));
+      A2D_TRY(a2d_add_f32(c.dacc[st % 2], c.part, (int64_t)kv_elems, s));
+    }
+    // next consumer: (r, p+1) inside an outer step, the diagonal (r+1, p+1) across and home
+    const bool diag = last || (st + 1) % c.w == 0;
+    const int to = diag ? c.diag_to : c.inner_to, from = diag ? c.diag_from : c.inner_from;
+    const void* src = c.dacc[st % 2];
+    size_t bytes = kv_elems * 4;
+    void* dst = last ? c.dkv_home : c.dacc[(st + 1) % 2];
+    if (last && hb) {
+      A2D_TRY(a2d_f32_to_bf16(c.dacc[st % 2], c.dkv_send, (int64_t)kv_elems, s));
+      src = c.dkv_send;
+      bytes = kv_elems * 2;
+    }
+    A2D_TRY(hop(c, c.c_dkv, c.s_dkv, s, src, to, dst, from, bytes, c.ev_dkv));
+    if (t + 1 < c.w) {
+      CUDA_TRY(cudaStreamWaitEvent(s, c.ev_inner, 0));
+      cur = nxt_inner;
+    } else if (!last) {
+      CUDA_TRY(cudaStreamWaitEvent(s, c.ev_outer, 0));
+      cur = first = nxt_outer;
+    }
+  }
+  CUDA_TRY(cudaStreamWaitEvent(s, c.ev_dkv, 0));
+  *home = c.dkv_home;
+  *home_bf16 = hb;
+  return A2D_OK;
+}
+
+int create(const void* id, int rank, int world, int d_hp, int d_cp, int w, int placement, int H, int Hkv, int d,
+           int64_t S, int causal, Ctx** out) {
+  if (d != 128) return set_error(A2D_EINVAL, "a2d_ctx_create: the native runtime supports head dim 128");
+  if (d_hp < 1 || d_cp < 1 || d_hp * d_cp != world) return set_error(A2D_EINVAL, "a2d_ctx_create: world != d_hp*d_cp");
+  if (w < 1 || d_cp % w) return set_error(A2D_EINVAL, "inner ring size " + std::to_string(w) + " must divide d_cp=" + std::to_string(d_cp));
+  if (H <= 0 || Hkv <= 0 || H % Hkv) return set_error(A2D_EINVAL, "a2d_ctx_create: H must be a multiple of H_kv");
+  if (d_hp > H) return set_error(A2D_EINVAL, "d_hp=" + std::to_string(d_hp) + " exceeds H=" + std::to_string(H));
+  if (H % d_hp) return set_error(A2D_EINVAL, "a2d_ctx_create: H not divisible by d_hp");
+  if (S <= 0 || S % (2 * world)) return set_error(A2D_EINVAL, "a2d_ctx_create: S must be divisible by 2*d_hp*d_cp");
+  Ctx* c = new Ctx();
+  *out = c;
+  c->rank = rank; c->world = world; c->d_hp = d_hp; c->d_cp = d_cp; c->w = w; c->placement = placement;
+  c->H = H; c->Hkv = Hkv; c->d = d; c->S = S; c->causal = causal;
+  c->H_rep = d_hp <= Hkv ? Hkv : std::lcm(Hkv, d_hp);
+  if (c->H_rep % d_hp) return set_error(A2D_EINVAL, "a2d_ctx_create: replicated KV heads not divisible by d_hp");
+  c->rep = c->H_rep / Hkv;
+  c->Hl = H / d_hp; c->Hkl = c->H_rep / d_hp;
+  c->L = S / world; c->C = S / d_cp; c->C_pad = (c->C + 63) / 64 * 64;
+  c->n_outer = d_cp / w;
+  c->scale = 1.0f / sqrtf((float)d);
+  if (placement == 0) { c->cp = rank / d_hp; c->hp = rank % d_hp; }  // head-first: rank = hp + d_hp*cp
+  else { c->hp = rank / d_cp; c->cp = rank % d_cp; }                 // context-first: rank = cp + d_cp*hp
+  // ---- communicators (ncclCommSplit keeps the key order: HP rank = hp, ring rank = cp)
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  NCCL_TRY(ncclCommInitRank(&c->world_comm, world, uid, rank));
+  NCCL_TRY(ncclCommSplit(c->world_comm, c->cp, c->hp, &c->hp_comm, nullptr));
+  NCCL_TRY(ncclCommSplit(c->world_comm, c->hp, c->cp, &c->c_inner, nullptr));
+  NCCL_TRY(ncclCommSplit(c->world_comm, c->hp, c->cp, &c->c_outer, nullptr));
+  NCCL_TRY(ncclCommSplit(c->world_comm, c->hp, c->cp, &c->c_dkv, nullptr));
+  for (cudaStream_t* s : {&c->s_inner, &c->s_outer, &c->s_dkv}) CUDA_TRY(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c->ev_ready, &c->ev_inner, &c->ev_outer, &c->ev_dkv})
+    CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  // ---- schedule and peers (schedule.build_ring_schedule / ring_peers)
+  const int n = c->n_outer, j = c->cp;
+  for (int o = 0; o < n; ++o)
+    for (int t = 0; t < w; ++t) c->steps.push_back({src_of(j, o, t, w, n), t, o});
+  auto idx = [&](int r, int p) { return ((r % n + n) % n) * w + ((p % w + w) % w); };
+  const int ring_i = j / w, pos_i = j % w;
+  c->inner_to = idx(ring_i, pos_i + 1); c->inner_from = idx(ring_i, pos_i - 1);
+  c->outer_to = idx(ring_i + 1, pos_i); c->outer_from = idx(ring_i - 1, pos_i);
+  c->diag_to = idx(ring_i + 1, pos_i + 1); c->diag_from = idx(ring_i - 1, pos_i - 1);
+  // ---- positions and tile bounds of every CP chunk
+  const int64_t C = c->C;
+  for (int jj = 0; jj < d_cp; ++jj) {
+    std::vector<int32_t> hpos = cp_positions(S, d_cp, jj);
+    int32_t *p = nullptr, *b1 = nullptr, *b2 = nullptr;
+    A2D_TRY(dalloc(*c, &p, C));
+    A2D_TRY(dalloc(*c, &b1, 2 * ((C + 127) / 128)));
+    A2D_TRY(dalloc(*c, &b2, 2 * ((C + 63) / 64)));
+    CUDA_TRY(cudaMemcpy(p, hpos.data(), C * 4, cudaMemcpyHostToDevice));
+    A2D_TRY(a2d_tile_bounds(p, C, 128, b1, nullptr));
+    A2D_TRY(a2d_tile_bounds(p, C, 64, b2, nullptr));
+    c->pos.push_back(p); c->b128.push_back(b1); c->b64.push_back(b2);
+  }
+  // ---- KV pack maps: block (peer, t, hl) of [d_hp][2][Hkl] reads source head (peer*Hkl + hl) / rep
+  std::vector<int32_t> sm, dk, dv;
+  for (int p = 0; p < d_hp; ++p)
+    for (int hl = 0; hl < c->Hkl; ++hl) {
+      sm.push_back((p * c->Hkl + hl) / c->rep);
+      dk.push_back(p * 2 * c->Hkl + hl);
+      dv.push_back(p * 2 * c->Hkl + c->Hkl + hl);
+    }
+  A2D_TRY(dalloc(*c, &c->smap, sm.size()));
+  A2D_TRY(dalloc(*c, &c->dmap_k, dk.size()));
+  A2D_TRY(dalloc(*c, &c->dmap_v, dv.size()));
+  CUDA_TRY(cudaMemcpy(c->smap, sm.data(), sm.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->dmap_k, dk.data(), dk.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->dmap_v, dv.data(), dv.size() * 4, cudaMemcpyHostToDevice));
+  // ---- buffers
+  const size_t qe = (size_t)c->Hl * C * 128, kve = (size_t)2 * c->Hkl * C * 128;
+  A2D_TRY(dalloc(*c, &c->kvh, kve));
+  if (d_hp > 1) {
+    A2D_TRY(dalloc(*c, &c->kv_send, kve));
+    A2D_TRY(dalloc(*c, &c->q_recv, qe));
+    A2D_TRY(dalloc(*c, &c->kv_recv, kve));
+    A2D_TRY(dalloc(*c, &c->qh_own, qe));
+    A2D_TRY(dalloc(*c, &c->g_send, std::max(qe, kve / 2)));
+  }
+  A2D_TRY(dalloc(*c, &c->out_h, qe));
+  if (d_hp > 1) A2D_TRY(dalloc(*c, &c->doh, qe));
+  A2D_TRY(dalloc(*c, &c->lse, (size_t)c->Hl * C));
+  A2D_TRY(dalloc(*c, &c->lse2, (size_t)c->Hl * c->C_pad));
+  A2D_TRY(dalloc(*c, &c->delta, (size_t)c->Hl * c->C_pad));
+  A2D_TRY(dalloc(*c, &c->dq_acc, (size_t)c->Hl * 128 * c->C_pad));
+  A2D_TRY(dalloc(*c, &c->dkv, kve));
+  if (d_cp > 1) {
+    A2D_TRY(dalloc(*c, &c->acc, qe));
+    for (auto& r : c->ring) A2D_TRY(dalloc(*c, &r, kve));
+    A2D_TRY(dalloc(*c, &c->part, kve));
+    A2D_TRY(dalloc(*c, &c->dacc[0], kve));
+    A2D_TRY(dalloc(*c, &c->dacc[1], kve));
+    A2D_TRY(dalloc(*c, &c->dkv_send, kve));
+    float* home = nullptr;
+    A2D_TRY(dalloc(*c, &home, kve));  // fp32-sized: also holds the bf16 home hop
+    c->dkv_home = home;
+  }
+  if (c->rep > 1) {
+    const size_t ge = (size_t)c->Hkl * C * 128;  // = H_rep * L * 128
+    A2D_TRY(dalloc(*c, &c->g32_send, ge));
+    A2D_TRY(dalloc(*c, &c->g32_recv, ge));
+    A2D_TRY(dalloc(*c, &c->g32_sum, (size_t)Hkv * c->L * 128));
+  }
+  CUDA_TRY(cudaDeviceSynchronize());
+  return A2D_OK;
+}
+
+int forward(Ctx& c, const void* q, const void* k, const void* v, void* out, cudaStream_t s) {
+  const size_t L128 = (size_t)c.L * 128;
+  // KV pack [peer][2][Hkl][L][128] (GQA replication by the head map), q needs none
+  // (d_hp = 1: the pack IS the HeadSharded KV chunk)
+  uint16_t* kvp = c.d_hp == 1 ? c.kvh : c.kv_send;
+  A2D_TRY(a2d_gather_blocks(k, kvp, c.smap, c.dmap_k, (int64_t)c.d_hp * c.Hkl, (int64_t)L128 * 2, s));
+  A2D_TRY(a2d_gather_blocks(v, kvp, c.smap, c.dmap_v, (int64_t)c.d_hp * c.Hkl, (int64_t)L128 * 2, s));
+  if (c.d_hp == 1) {
+    c.qh = static_cast<const uint16_t*>(q);
+  } else {
+    A2D_TRY(a2a(c, q, c.q_recv, (size_t)c.Hl * L128 * 2, s));
+    A2D_TRY(a2a(c, c.kv_send, c.kv_recv, (size_t)2 * c.Hkl * L128 * 2, s));
+    A2D_TRY(a2d_permute_blocks(c.q_recv, c.qh_own, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
+    A2D_TRY(a2d_permute_blocks(c.kv_recv, c.kvh, c.d_hp, 2 * c.Hkl, (int64_t)L128 * 2, s));
+    c.qh = c.qh_own;
+  }
+  A2D_TRY(ring_forward(c, s));
+  A2D_TRY(gather_bf16(c, c.out_h, c.Hl, static_cast<uint16_t*>(out), s));
+  c.have_state = true;
+  return A2D_OK;
+}
+
+int backward(Ctx& c, const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+  if (!c.have_state) return set_error(A2D_EINVAL, "a2d_bwd called before a2d_fwd");
+  const size_t L128 = (size_t)c.L * 128;
+  if (c.d_hp == 1) {
+    c.dO = static_cast<const uint16_t*>(dout);
+  } else {
+    A2D_TRY(a2a(c, dout, c.q_recv, (size_t)c.Hl * L128 * 2, s));
+    A2D_TRY(a2d_permute_blocks(c.q_recv, c.doh, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
+    c.dO = c.doh;
+  }
+  A2D_TRY(a2d_bwd_preprocess(c.out_h, c.dO, c.lse, c.Hl, c.C, 128, c.lse2, c.delta, s));
+  CUDA_TRY(cudaMemsetAsync(c.dq_acc, 0, (size_t)c.Hl * 128 * c.C_pad * 4, s));
+  const void* home = nullptr;
+  bool home_bf16 = false;
+  A2D_TRY(ring_backward(c, s, &home, &home_bf16));
+  // dQ: transposed accumulator -> bf16 peer-major pack -> all-to-all into the caller's dq
+  if (c.d_hp == 1) {
+    A2D_TRY(a2d_dqt_to_bf16(c.dq_acc, dq, c.Hl, c.C, c.C_pad, 1, s));
+  } else {
+    A2D_TRY(a2d_dqt_to_bf16(c.dq_acc, c.g_send, c.Hl, c.C, c.C_pad, c.d_hp, s));
+    A2D_TRY(a2a(c, c.g_send, dq, (size_t)c.Hl * L128 * 2, s));
+  }
+  const size_t half = (size_t)c.Hkl * c.C * 128;
+  void* outs[2] = {dk, dv};
+  for (int t = 0; t < 2; ++t) {
+    if (c.rep == 1) {
+      if (home_bf16) {
+        A2D_TRY(gather_bf16(c, static_cast<const uint16_t*>(home) + t * half, c.Hkl, static_cast<uint16_t*>(outs[t]), s));
+      } else {
+        A2D_TRY(gather_f32_to_bf16(c, static_cast<const float*>(home) + t * half, c.Hkl, static_cast<uint16_t*>(outs[t]), s));
+      }
+    } else {  // GQA replicas: gather fp32, sum the copies, round once
+      const float* src = static_cast<const float*>(home) + t * half;
+      A2D_TRY(a2d_permute_blocks(src, c.g32_send, c.Hkl, c.d_hp, (int64_t)L128 * 4, s));
+      A2D_TRY(a2a(c, c.g32_send, c.g32_recv, (size_t)c.Hkl * L128 * 4, s));
+      A2D_TRY(a2d_sum_replicas_f32(c.g32_recv, c.g32_sum, c.Hkv, c.rep, (int64_t)L128, s));
+      A2D_TRY(a2d_f32_to_bf16(c.g32_sum, outs[t], (int64_t)c.Hkv * L128, s));
+    }
+  }
+  return A2D_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int a2d_nccl_unique_id(void* out, int64_t out_bytes) {
+  if (out_bytes < (int64_t)sizeof(ncclUniqueId)) return set_error(A2D_EINVAL, "a2d_nccl_unique_id: buffer too small");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return A2D_OK;
+}
+
+int a2d_ctx_create(const void* nccl_id, int32_t rank, int32_t world, int32_t d_hp, int32_t d_cp, int32_t w,
+                   int32_t placement, int32_t H, int32_t H_kv, int32_t d, int64_t S, int32_t causal, void** ctx) {
+  Ctx* c = nullptr;
+  const int rc = create(nccl_id, rank, world, d_hp, d_cp, w, placement, H, H_kv, d, S, causal, &c);
+  if (rc) {
+    const std::string msg = a2d_last_error();
+    destroy(c);
+    *ctx = nullptr;
+    return set_error(rc, msg);
+  }
+  *ctx = c;
+  return A2D_OK;
+}
+
+int a2d_fwd(void* ctx, const void* q, const void* k, const void* v, void* out, void* stream) {
+  if (!ctx) return set_error(A2D_EINVAL, "a2d_fwd: null context");
+  return forward(*static_cast<Ctx*>(ctx), q, k, v, out, static_cast<cudaStream_t>(stream));
+}
+
+int a2d_bwd(void* ctx, const void* dout, void* dq, void* dk, void* dv, void* stream) {
+  if (!ctx) return set_error(A2D_EINVAL, "a2d_bwd: null context");
+  return backward(*static_cast<Ctx*>(ctx), dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+}
+
+int a2d_ctx_destroy(void* ctx) { return destroy(static_cast<Ctx*>(ctx)); }
+
+}  // extern "C"

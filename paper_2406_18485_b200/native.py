@@ -1,0 +1,75 @@
+"""torch face of the native SPMD runtime (C ABI a2d_ctx_create / a2d_fwd /
+a2d_bwd, csrc/runtime.cu): the whole 2D-attention layer of one rank, NCCL
+inside the library. Same tensors and layout as ``dist.Attn2D`` (head-major
+SeqSharded chunks in zig-zag order); torch.distributed only hands the NCCL id
+from rank 0 to the others."""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .config import ClusterConfig, ModelConfig, ParallelConfig, Placement, build_rank_grid, check_config
+
+
+class NativeAttn2D:
+    def __init__(self, model: ModelConfig, par: ParallelConfig, cluster: ClusterConfig | None = None,
+                 causal: bool = True):
+        check_config(model, par, cluster or ClusterConfig())
+        if model.head_dim != 128:
+            raise ValueError("the native runtime supports head dim 128")
+        self.model, self.par, self.causal = model, par, causal
+        self.grid = build_rank_grid(par, cluster or ClusterConfig())
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        if self.world != par.d_hp * par.d_cp:
+            raise ValueError(f"world size {self.world} != d_hp*d_cp = {par.d_hp * par.d_cp}")
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.call("a2d_nccl_unique_id", ctypes.addressof(uid), 128)
+        box = [uid.raw if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = ctypes.create_string_buffer(box[0], 128)
+        self._uid = uid
+        self._ctx = ctypes.c_void_p()
+        placement = 0 if par.placement is Placement.HEAD_FIRST else 1
+        _lib.call("a2d_ctx_create", ctypes.addressof(uid), self.rank, self.world, par.d_hp, par.d_cp,
+                  par.inner_ring, placement, model.heads, model.kv_heads, model.head_dim, model.seq_len,
+                  int(causal), ctypes.addressof(self._ctx))
+        self.L = model.seq_len // self.world
+        self._q = None
+
+    def _empty(self, heads: int, like: torch.Tensor) -> torch.Tensor:
+        return torch.empty((heads, self.L, self.model.head_dim), dtype=torch.bfloat16, device=like.device)
+
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+        m = self.model
+        for t, h in ((q, m.heads), (k, m.kv_heads), (v, m.kv_heads)):
+            if tuple(t.shape) != (h, self.L, m.head_dim) or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                raise ValueError(f"expected contiguous bf16 ({h}, {self.L}, {m.head_dim}), got {tuple(t.shape)}")
+        out = self._empty(m.heads, q)
+        self._q = q  # with d_hp = 1 the runtime keeps reading q in the backward
+        _lib.call("a2d_fwd", self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        return out
+
+    def backward(self, dout: torch.Tensor):
+        m = self.model
+        dout = dout.to(torch.bfloat16).contiguous()
+        dq, dk, dv = self._empty(m.heads, dout), self._empty(m.kv_heads, dout), self._empty(m.kv_heads, dout)
+        _lib.call("a2d_bwd", self._ctx, dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        return dq, dk, dv
+
+    def close(self) -> None:
+        if self._ctx:
+            _lib.call("a2d_ctx_destroy", self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

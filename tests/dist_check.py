@@ -47,6 +47,9 @@ def main():
     ap.add_argument("--fused-qkv", action="store_true",
                     help="token-major (L, H+2H_kv, d) fused QKV buffer, q/k/v passed as strided views, "
                          "gradients through torch.autograd (Attn2DFunction)")
+    ap.add_argument("--native", action="store_true",
+                    help="run the native C++ runtime (C ABI a2d_ctx_create/a2d_fwd/a2d_bwd) instead of dist.Attn2D, "
+                         "and also compare it with dist.Attn2D")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
@@ -79,6 +82,18 @@ def main():
         g = qkv.grad
         dq, dk, dv = (g[:, lo:hi].transpose(0, 1).contiguous()
                       for lo, hi in ((0, H), (H, H + Hkv), (H + Hkv, H + 2 * Hkv)))
+    elif a.native:
+        from paper_2406_18485_b200.native import NativeAttn2D
+        nat = NativeAttn2D(model, par, ClusterConfig(), causal=bool(a.causal))
+        args = [shard_global(x, op) for x in (qt, kt, vt)]
+        out = nat.forward(*args)
+        dq, dk, dv = nat.backward(shard_global(dot, op))
+        ref_out = op.forward(*args)
+        ref_grads = op.backward(shard_global(dot, op))
+        torch.cuda.synchronize()
+        vs_py = max(float((a_.float() - b_.float()).abs().max() / max(1.0, float(b_.float().abs().max())))
+                    for a_, b_ in zip((out, dq, dk, dv), (ref_out,) + tuple(ref_grads)))
+        nat.close()
     else:
         out = op.forward(shard_global(qt, op), shard_global(kt, op), shard_global(vt, op))
         dq, dk, dv = op.backward(shard_global(dot, op))
@@ -105,6 +120,8 @@ def main():
             res["dQ"], res["dK"], res["dV"] = metrics(DQ, rq), metrics(DK, rk), metrics(DV, rv)
         res["config"] = vars(a)
         res["head_groups"] = op.ng
+        if a.native:
+            res["native_vs_python"] = vs_py
         print(json.dumps(res))
         if a.out:
             with open(a.out, "w") as f:

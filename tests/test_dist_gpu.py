@@ -47,12 +47,12 @@ def test_dist_non_causal(tmp_path):
             f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
 
 
-def _run(nproc, args, tmp_path, env=None):
+def _run(nproc, args, tmp_path, env=None, timeout=600):
     out = tmp_path / "res.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "dist_check.py"),
            *args, "--out", str(out)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT,
                        env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return json.loads(out.read_text())
@@ -164,3 +164,33 @@ def test_dist_pipelined_head_groups(case, tmp_path):
         ma, rl, rng = res[name]
         assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
             f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
+
+
+NATIVE = [
+    # d_hp, d_cp, w, placement, H, H_kv, S
+    (1, 1, 1, "head_first", 4, 2, 1024),
+    (2, 1, 1, "head_first", 8, 8, 1024),
+    (1, 2, 2, "context_first", 8, 4, 1024),
+    (2, 2, 1, "head_first", 8, 8, 2048),
+    (1, 4, 2, "head_first", 4, 4, 2048),
+    (4, 1, 1, "context_first", 8, 2, 1024),   # GQA replication (H_kv < d_hp)
+    (2, 2, 2, "head_first", 4, 1, 1024),      # replication and a ring: fp32 home hop
+]
+
+
+@pytest.mark.parametrize("case", NATIVE, ids=lambda c: "x".join(map(str, c[:3])) + f"-{c[3]}-H{c[4]}-{c[5]}")
+def test_native_runtime_matches_oracle_and_python(case, tmp_path):
+    """Native C++ runtime behind the context C ABI: same parity bar
+    as the Python runtime, and the same numbers as dist.Attn2D (NCCL transport)."""
+    d_hp, d_cp, w, pl, H, Hkv, S = case
+    n = d_hp * d_cp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    res = _run(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
+                   "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", "128", "--native"],
+               tmp_path, env={"A2D_TRANSPORT": "nccl"}, timeout=180)
+    for name in ("O", "dQ", "dK", "dV"):
+        ma, rl, rng = res[name]
+        assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
+            f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
+    assert res["native_vs_python"] <= 1e-2, res["native_vs_python"]
