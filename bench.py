@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--runtime", default="python", choices=["python", "native"],
+                    help="python: dist.Attn2D (default); native: the C++ runtime behind a2d_ctx_create/a2d_fwd/a2d_bwd")
     ap.add_argument("--seq", type=int, default=131072)
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=32)
@@ -251,6 +253,11 @@ def main():
     model = ModelConfig(seq_len=S, heads=H, kv_heads=Hkv, hidden=H * d)
     par = ParallelConfig(d_hp=d_hp, d_cp=d_cp, inner_ring=w, placement=Placement(a.placement))
     op = Attn2D(model, par, ClusterConfig(), causal=True)
+    if a.runtime == "native":
+        from paper_2406_18485_b200.native import NativeAttn2D
+        run = NativeAttn2D(model, par, ClusterConfig(), causal=True)
+    else:
+        run = op
     L = op.L
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     q = torch.randn((H, L, d), device=dev, dtype=torch.bfloat16, generator=g)
@@ -259,8 +266,8 @@ def main():
     do = torch.randn((H, L, d), device=dev, dtype=torch.bfloat16, generator=g)
 
     def step():
-        op.forward(q, k, v)
-        return op.backward(do)
+        run.forward(q, k, v)
+        return run.backward(do)
 
     for _ in range(max(a.warmup, 3 if a.warmup >= 3 else a.warmup)):
         step()
@@ -301,7 +308,7 @@ def main():
     # ---------------- exposed communication: same step with every NCCL call
     # skipped (kernels and buffers identical), max over ranks
     exposed = None
-    if world > 1:
+    if world > 1 and a.runtime == "python":
         op.comm_enabled = False
         step()
         torch.cuda.synchronize()
@@ -365,9 +372,9 @@ def main():
                         if ev_done[nxt] is not None:
                             cs.wait_event(ev_done[nxt])  # step i-1 finished reading that buffer set
                         load(nxt)
-                op.forward(dev_in[cur][0], dev_in[cur][1], dev_in[cur][2])
+                run.forward(dev_in[cur][0], dev_in[cur][1], dev_in[cur][2])
                 main.wait_event(ev_do[cur])
-                grads = op.backward(dev_in[cur][3])
+                grads = run.backward(dev_in[cur][3])
                 ev = torch.cuda.Event()
                 ev.record(main)
                 ev_done[cur] = ev
@@ -432,7 +439,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random bf16 q/k/v/dO)",
-            "config": workload_config(a, world),
+            "config": {**workload_config(a, world), **({"runtime": "native C++ (a2d_ctx_create/a2d_fwd/a2d_bwd)"}
+                                                         if a.runtime == "native" else {})},
             "tflops_per_gpu": per_gpu, "mfu": per_gpu / pk["bf16_tflops"],
             "mfu_sustained": per_gpu / pk["bf16_tflops_sustained"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
