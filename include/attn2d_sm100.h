@@ -145,6 +145,14 @@ int a2d_fwd(void* ctx, const void* q, const void* k, const void* v, void* out, v
 /* Backward of the last a2d_fwd: dq, dk, dv SeqSharded bf16. Collective. */
 int a2d_bwd(void* ctx, const void* dout, void* dq, void* dk, void* dv, void* stream);
 int a2d_ctx_destroy(void* ctx);
+/* Host-side plan of the native runtime, exposed for tests and other hosts:
+ * CP rank j's ring schedule as (source, outer step, inner step) triples
+ * (d_cp of them, ref build_ring_schedule ring.py:41-61) and its peers
+ * (inner_to, inner_from, outer_to, outer_from, diag_to, diag_from); and the
+ * zig-zag token positions of CP chunk j (ref zigzag_reorder sharding.py:33-53).
+ * No GPU needed. */
+int a2d_ring_plan(int32_t d_cp, int32_t w, int32_t j, int32_t* steps_out, int32_t* peers_out);
+int a2d_zigzag_positions(int64_t S, int32_t d_cp, int32_t j, int32_t* out);
 
 /* UMMA plumbing self-test (one CTA, 128x128x128 bf16 GEMMs in four operand
  * layouts); c is fp32 [4][128][128]. Used by the parity tests. */

@@ -92,6 +92,20 @@ int src_of(int j, int o, int t, int w, int n) {  // ring.py:53-59
   return ((ring - o) % n + n) % n * w + ((pos - t) % w + w) % w;
 }
 
+// CP rank j's schedule (schedule.build_ring_schedule) and peers
+// (schedule.ring_peers): inner_to, inner_from, outer_to, outer_from, diag_to, diag_from
+void ring_plan(int d_cp, int w, int j, std::vector<Step>* steps, int peers[6]) {
+  const int n = d_cp / w;
+  steps->clear();
+  for (int o = 0; o < n; ++o)
+    for (int t = 0; t < w; ++t) steps->push_back({src_of(j, o, t, w, n), t, o});
+  auto idx = [&](int r, int p) { return ((r % n + n) % n) * w + ((p % w + w) % w); };
+  const int ring = j / w, pos = j % w;
+  const int v[6] = {idx(ring, pos + 1), idx(ring, pos - 1), idx(ring + 1, pos),
+                    idx(ring - 1, pos), idx(ring + 1, pos + 1), idx(ring - 1, pos - 1)};
+  std::copy(v, v + 6, peers);
+}
+
 // grouped send/recv of bytes_per_peer to/from every member of the HP group
 int a2a(Ctx& c, const void* send, void* recv, size_t bytes_per_peer, cudaStream_t s) {
   NCCL_TRY(ncclGroupStart());
@@ -296,14 +310,10 @@ int create(const void* id, int rank, int world, int d_hp, int d_cp, int w, int p
   for (cudaEvent_t* e : {&c->ev_ready, &c->ev_inner, &c->ev_outer, &c->ev_dkv})
     CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   // ---- schedule and peers (schedule.build_ring_schedule / ring_peers)
-  const int n = c->n_outer, j = c->cp;
-  for (int o = 0; o < n; ++o)
-    for (int t = 0; t < w; ++t) c->steps.push_back({src_of(j, o, t, w, n), t, o});
-  auto idx = [&](int r, int p) { return ((r % n + n) % n) * w + ((p % w + w) % w); };
-  const int ring_i = j / w, pos_i = j % w;
-  c->inner_to = idx(ring_i, pos_i + 1); c->inner_from = idx(ring_i, pos_i - 1);
-  c->outer_to = idx(ring_i + 1, pos_i); c->outer_from = idx(ring_i - 1, pos_i);
-  c->diag_to = idx(ring_i + 1, pos_i + 1); c->diag_from = idx(ring_i - 1, pos_i - 1);
+  int peers[6];
+  ring_plan(d_cp, w, c->cp, &c->steps, peers);
+  c->inner_to = peers[0]; c->inner_from = peers[1]; c->outer_to = peers[2];
+  c->outer_from = peers[3]; c->diag_to = peers[4]; c->diag_from = peers[5];
   // ---- positions and tile bounds of every CP chunk
   const int64_t C = c->C;
   for (int jj = 0; jj < d_cp; ++jj) {
@@ -470,5 +480,28 @@ int a2d_bwd(void* ctx, const void* dout, void* dq, void* dk, void* dv, void* str
 }
 
 int a2d_ctx_destroy(void* ctx) { return destroy(static_cast<Ctx*>(ctx)); }
+
+int a2d_ring_plan(int32_t d_cp, int32_t w, int32_t j, int32_t* steps_out, int32_t* peers_out) {
+  if (d_cp < 1 || w < 1 || d_cp % w || j < 0 || j >= d_cp)
+    return set_error(A2D_EINVAL, "a2d_ring_plan: need 0 <= j < d_cp and w | d_cp");
+  std::vector<Step> steps;
+  int peers[6];
+  ring_plan(d_cp, w, j, &steps, peers);
+  for (size_t i = 0; i < steps.size(); ++i) {
+    steps_out[3 * i] = steps[i].source;
+    steps_out[3 * i + 1] = steps[i].outer;
+    steps_out[3 * i + 2] = steps[i].inner;
+  }
+  std::copy(peers, peers + 6, peers_out);
+  return A2D_OK;
+}
+
+int a2d_zigzag_positions(int64_t S, int32_t d_cp, int32_t j, int32_t* out) {
+  if (d_cp < 1 || S <= 0 || S % (2 * d_cp) || j < 0 || j >= d_cp)
+    return set_error(A2D_EINVAL, "a2d_zigzag_positions: need S divisible by 2*d_cp and 0 <= j < d_cp");
+  const std::vector<int32_t> p = cp_positions(S, d_cp, j);
+  std::copy(p.begin(), p.end(), out);
+  return A2D_OK;
+}
 
 }  // extern "C"

@@ -262,3 +262,30 @@ def test_symm_exchange_layout_fits_and_is_disjoint(d_hp, Hl, Hkl, ng):
     # scatters use the IN region, gathers the OUT region
     assert all(o + b <= op._in_bytes for o, b in phases[0] + phases[1])
     assert all(o >= op._in_bytes for o, _ in phases[2] + phases[3])
+
+
+@pytest.mark.parametrize("d_cp,w", [(1, 1), (2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 2), (8, 4), (16, 4), (12, 3)])
+def test_native_ring_plan_matches_schedule(d_cp, w):
+    """The native runtime's C++ ring plan (a2d_ring_plan) equals schedule.py's
+    schedule and peers, and its zig-zag positions equal layout.cp_positions."""
+    import ctypes
+    import numpy as np
+    from paper_2406_18485_b200 import _lib
+    from paper_2406_18485_b200.layout import cp_positions
+    from paper_2406_18485_b200.schedule import build_ring_schedule, ring_peers
+    sched = build_ring_schedule(d_cp, w)
+    S = 48 * d_cp
+    for j in range(d_cp):
+        steps = (ctypes.c_int32 * (3 * d_cp))()
+        peers = (ctypes.c_int32 * 6)()
+        _lib.call("a2d_ring_plan", d_cp, w, j, ctypes.addressof(steps), ctypes.addressof(peers))
+        want = [(st.source, st.outer, st.inner) for st in sched.steps[j]]
+        got = [tuple(steps[3 * i:3 * i + 3]) for i in range(d_cp)]
+        assert got == want, (j, got, want)
+        p = ring_peers(j, d_cp, w)
+        assert list(peers) == [p.inner_to, p.inner_from, p.outer_to, p.outer_from, p.diag_to, p.diag_from]
+        pos = np.zeros(S // d_cp, dtype=np.int32)
+        _lib.call("a2d_zigzag_positions", S, d_cp, j, pos.ctypes.data)
+        assert np.array_equal(pos, cp_positions(S, d_cp, j))
+    with pytest.raises(ValueError):
+        _lib.call("a2d_ring_plan", d_cp, d_cp + 1, 0, ctypes.addressof(steps), ctypes.addressof(peers))
