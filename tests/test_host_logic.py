@@ -289,3 +289,24 @@ def test_native_ring_plan_matches_schedule(d_cp, w):
         assert np.array_equal(pos, cp_positions(S, d_cp, j))
     with pytest.raises(ValueError):
         _lib.call("a2d_ring_plan", d_cp, d_cp + 1, 0, ctypes.addressof(steps), ctypes.addressof(peers))
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the driver's reference arm) prints one JSON
+    line with the contract's fields, on the same config object as our arm."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--seq", "4096", "--cpu-rows", "64"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert line["config"]["workload"].startswith("2D-Attention fwd+bwd") and line["config"]["global_tokens"] == 4096
