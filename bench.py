@@ -205,6 +205,79 @@ def run_reference(a, rank: int, world: int):
     return 0
 
 
+HBM_KERNELS = ("a2d_bwd_preprocess", "a2d_dqt_to_bf16", "a2d_permute_blocks", "a2d_gather_blocks",
+               "a2d_permute_f32_to_bf16", "a2d_copy_rows", "a2d_merge", "a2d_add_f32", "a2d_f32_to_bf16",
+               "a2d_sum_replicas_f32")
+
+
+def hbm_roofline(events, peak_gbs: float) -> dict:
+    """Per HBM-bound kernel: algorithmic bytes (read + write of every element
+    moved, from the wrappers in kernels.py) / CUDA-event time on the launching
+    stream, summed over the timed region."""
+    acc: dict = {}
+    for name, s0, s1, nbytes in events:
+        if name not in HBM_KERNELS:
+            continue
+        e = acc.setdefault(name, [0, 0.0, 0])
+        e[0] += 1
+        e[1] += s0.elapsed_time(s1)
+        e[2] += nbytes
+    out = {}
+    for name, (n, ms, nb) in sorted(acc.items()):
+        gbs = nb / (ms * 1e-3) / 1e9 if ms > 0 else None
+        out[name] = {"calls": n, "bytes": nb, "ms": ms, "gbs": gbs, "peak": peak_gbs,
+                     "frac": gbs / peak_gbs if gbs else None}
+    return out
+
+
+def parity_check(a, run, op, q, k, v, do, world, rank):
+    """Sampled f64-oracle parity of one step of the benched configuration on
+    the benched inputs (oracle/sampled.py; checker only, outside every timed
+    region). Gathers the SeqSharded tensors of all ranks to global order."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_18485_b200.dist import unshard_global
+
+    out = run.forward(q, k, v)
+    dq, dk, dv = run.backward(do)
+    lse = op.saved[3].contiguous() if run is op and op.saved is not None else None
+    torch.cuda.synchronize()
+
+    def glob(x):
+        if world == 1:
+            return unshard_global([x], op)
+        parts = [torch.empty_like(x) for _ in range(world)]
+        dist.all_gather(parts, x.contiguous())
+        return unshard_global(parts, op)
+
+    G = [glob(x) for x in (q, k, v, do, out, dq, dk, dv)]
+    LSE = None
+    if lse is not None:
+        parts = [lse] if world == 1 else [torch.empty_like(lse) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(parts, lse)
+        LSE = torch.empty((a.heads, a.seq), dtype=torch.float32, device=lse.device)
+        for r, part in enumerate(parts):
+            hp, cp = op.grid.coords_of(r)
+            LSE[hp * op.Hl:(hp + 1) * op.Hl][:, op.plans[cp].pos.long()] = part
+    res = None
+    if rank == 0:
+        from oracle import sampled
+        t0 = time.perf_counter()
+        res = sampled.check(*G, LSE, causal=True, n_rows=512, n_keys=256, seed=7)
+        res["violations"] = sampled.passes(res)
+        res["seconds"] = time.perf_counter() - t0
+        res["bar"] = ("per tensor [max_abs, rel_l2, max|ref|, excess]: rel-L2 <= 1e-2 and max-abs <= 2e-2 beyond "
+                      "one bf16 ulp of |ref| for bf16 outputs (= the plain absolute bar where |ref| < ~5); "
+                      "f64 row stats pinned <= 1e-9")
+        res["sample"] = (f"{res['rows']} query rows x heads {res['heads']} (O, LSE, dQ), {res['keys']} keys "
+                         f"(dK, dV) of this run's inputs, f64 oracle")
+    del G
+    torch.cuda.empty_cache()
+    return res
+
+
 # ------------------------------------------------------------------ GPU leg
 def main():
     ap = argparse.ArgumentParser()
@@ -225,6 +298,10 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--check", dest="check", action="store_true", default=True,
+                    help="(default) after timing, check this run's O/LSE/dQ on sampled rows and dK/dV on sampled "
+                         "keys against the f64 oracle (oracle/sampled.py) and report them under 'parity'")
+    ap.add_argument("--no-check", dest="check", action="store_false")
     a = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -277,8 +354,9 @@ def main():
     # ---------------- timed region: inputs resident in HBM
     clocks = ClockSampler(local)
     clocks.start()
-    _lib.LOG.reset(timed=("a2d_fa_bwd_chunk", "a2d_fa_fwd_chunk"))
+    _lib.LOG.reset(timed=("a2d_fa_bwd_chunk", "a2d_fa_fwd_chunk") + HBM_KERNELS)
     _lib.LOG.enabled = True
+    n_launch0 = _lib.launch_count()
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -288,14 +366,16 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     _lib.LOG.enabled = False
+    launches = _lib.launch_count() - n_launch0  # our kernels launched in the timed region (C-side counter)
     dist.barrier()
     clk = clocks.stop()
     t_ms = e0.elapsed_time(e1)
-    launches = _lib.LOG.count            # our kernels launched in the timed region (all K steps)
     kern = {"a2d_fa_bwd_chunk": [0.0, 0], "a2d_fa_fwd_chunk": [0.0, 0]}
-    for name, s0, s1 in _lib.LOG.events:
-        kern[name][0] += s0.elapsed_time(s1)
-        kern[name][1] += 1
+    for name, s0, s1, _ in _lib.LOG.events:
+        if name in kern:
+            kern[name][0] += s0.elapsed_time(s1)
+            kern[name][1] += 1
+    hbm = hbm_roofline(_lib.LOG.events, peaks()["hbm_gbs"])
     tt = torch.tensor([t_ms, kern["a2d_fa_bwd_chunk"][0], kern["a2d_fa_fwd_chunk"][0]], device=dev,
                       dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -403,6 +483,13 @@ def main():
                "pipelining": "side copy stream: H2D of step i+1 and D2H of step i overlap step i+1 compute; "
                               "dO's H2D overlaps the forward of its own step"}
 
+    parity = None
+    if a.check:
+        try:
+            parity = parity_check(a, run, op, q, k, v, do, world, rank)
+        except Exception as exc:  # report, never lose the bench line
+            parity = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank == 0:
         pk = peaks()
         per_gpu = value / world
@@ -445,7 +532,7 @@ def main():
             "mfu_sustained": per_gpu / pk["bf16_tflops_sustained"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / a.steps,
-            "clocks": clk, "exposed_comm": exposed,
+            "clocks": clk, "exposed_comm": exposed, "hbm_roofline": hbm, "parity": parity,
         }
         print(json.dumps(line))
     dist.barrier()

@@ -30,11 +30,16 @@ extern "C" {
 #define A2D_OK 0
 #define A2D_EINVAL 1
 #define A2D_ECUDA 2
+#define A2D_ETIMEOUT 3
 
 /* Thread-local message of the last failing call. */
 const char* a2d_last_error(void);
 /* ABI version (bumped on any signature change). */
 int a2d_abi_version(void);
+/* Process-wide count of CUDA kernels this library has launched (every entry
+ * point below, including those the native runtime calls internally). The
+ * bench reads it around its timed region. */
+long long a2d_launch_count(void);
 
 /* Per-tile (min, max) of positions: out[2*t], out[2*t+1] for tile t of
  * `tile` tokens; empty tiles get (INT_MAX, INT_MIN). Input to the
@@ -129,9 +134,13 @@ int a2d_add_f32(float* dst, const float* src, int64_t n, void* stream);
  * reference's RankGrid (config.py:155-163). Tensors are this rank's
  * SeqSharded chunks, head-major bf16 device arrays: q/out/dout/dq [H][L][d],
  * k/v/dk/dv [H_kv][L][d], L = S/(d_hp*d_cp), tokens in zig-zag order (ref
- * shard_sequence, sharding.py:56-79). Head dim 128. One forward in flight per
- * context; its state is kept for the next a2d_bwd (with d_hp = 1 the caller's
- * q must stay valid until then). */
+ * shard_sequence, sharding.py:56-79). Head dim 128.
+ * Stateless contexts: a forward's state (HeadSharded Q, K/V chunk, output and
+ * natural-log LSE — what the backward needs) is written into a CALLER-OWNED
+ * `saved` buffer, so any number of layers / micro-batches can be in flight
+ * (the reference operator is a pure function, ring.py:82-119). The context
+ * owns only workspaces, reused in stream order: calls on one context must be
+ * issued on one stream (or ordered by the caller). */
 /* Rank 0 creates the NCCL id (128 bytes) and shares it with the other ranks. */
 int a2d_nccl_unique_id(void* out, int64_t out_bytes);
 /* Collective over all `world` ranks: communicators (HP all-to-all group; inner,
@@ -139,11 +148,24 @@ int a2d_nccl_unique_id(void* out, int64_t out_bytes);
  * buffers. Replaces run_2d_attention's setup (ring.py:82-107). */
 int a2d_ctx_create(const void* nccl_id, int32_t rank, int32_t world, int32_t d_hp, int32_t d_cp, int32_t w,
                    int32_t placement, int32_t H, int32_t H_kv, int32_t d, int64_t S, int32_t causal, void** ctx);
+/* Size of the saved-state buffer one a2d_fwd fills for its a2d_bwd. Layout
+ * (256-byte aligned regions, C = S/d_cp, Hl = H/d_hp, Hkl = replicated KV
+ * heads/d_hp): Q [Hl][C][128] bf16 | K,V [2][Hkl][C][128] bf16 |
+ * out [Hl][C][128] bf16 | LSE [Hl][C] fp32 (natural log, ref oracle.py:94). */
+int a2d_saved_bytes(void* ctx, int64_t* bytes);
 /* Forward of the layer (ref run_2d_attention, ring.py:82-119): out = this
- * rank's SeqSharded output. Collective; stream-ordered on `stream`. */
-int a2d_fwd(void* ctx, const void* q, const void* k, const void* v, void* out, void* stream);
-/* Backward of the last a2d_fwd: dq, dk, dv SeqSharded bf16. Collective. */
-int a2d_bwd(void* ctx, const void* dout, void* dq, void* dk, void* dv, void* stream);
+ * rank's SeqSharded output; `saved` (256-byte aligned, a2d_saved_bytes) gets
+ * this call's state. Collective; stream-ordered on `stream`. */
+int a2d_fwd(void* ctx, const void* q, const void* k, const void* v, void* out, void* saved, void* stream);
+/* Backward of the a2d_fwd that filled `saved`: dq, dk, dv SeqSharded bf16.
+ * Collective. `saved` is only read. */
+int a2d_bwd(void* ctx, const void* saved, const void* dout, void* dq, void* dk, void* dv, void* stream);
+/* Wait for `stream` while polling every communicator of the context with
+ * ncclCommGetAsyncError. On an NCCL error, or after timeout_ms (< 0: none),
+ * abort the communicators (ncclCommAbort: no rank hangs on a dead peer) and
+ * return A2D_ECUDA / A2D_ETIMEOUT; the context then refuses further calls
+ * and only a2d_ctx_destroy is valid. */
+int a2d_sync(void* ctx, void* stream, int64_t timeout_ms);
 int a2d_ctx_destroy(void* ctx);
 /* Host-side plan of the native runtime, exposed for tests and other hosts:
  * CP rank j's ring schedule as (source, outer step, inner step) triples

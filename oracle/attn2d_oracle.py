@@ -134,6 +134,52 @@ def attention_grads(q, k, v, d_out, q_pos, k_pos, causal=False):
     return dq, dk_r.reshape(fold).sum(axis=1), dv_r.reshape(fold).sum(axis=1)
 
 
+def attention_grads_rows(q, k, v, d_out_rows, q_pos, k_pos, rows, causal=False):
+    """dQ restricted to query rows ``rows`` — ref ``attention_backward``
+    (oracle.py:127-152) evaluated on those rows only. Exact: every quantity of a
+    dQ row (P, dP = dO V^T, row = sum(dP*P) at oracle.py:145, dS, dS K) depends
+    on that row alone. ``d_out_rows`` is (H, len(rows), d)."""
+    q = np.asarray(q, np.float64)[:, rows]
+    k = np.asarray(k, np.float64)
+    v = np.asarray(v, np.float64)
+    do = np.asarray(d_out_rows, np.float64)
+    g = _group(q.shape[0], k.shape[0])
+    scale = 1.0 / math.sqrt(q.shape[-1])
+    p, _ = _softmax_lse(_masked_scores(q, k, np.asarray(q_pos)[rows], k_pos, causal))
+    kk = np.repeat(k, g, axis=0)
+    dp = np.matmul(do, np.repeat(v, g, axis=0).transpose(0, 2, 1))
+    ds = p * (dp - (dp * p).sum(axis=-1, keepdims=True))
+    return np.matmul(ds, kk) * scale
+
+
+def attention_key_grads(q, k, v, d_out, q_pos, k_pos, keys, lse, delta, causal=False):
+    """(dK, dV) restricted to key columns ``keys`` — ref ``attention_backward``
+    (oracle.py:127-152) on those columns. A key column needs every query row's
+    softmax statistics: ``lse`` (H, Tq) natural log (= the oracle's LSE) and
+    ``delta`` (H, Tq) = rowsum(dP*P) (oracle.py:145; equals rowsum(dO*O)). With
+    those given, P[:, keys] = exp(S[:, keys] - lse) is exact, and
+    dK = dS^T Q / sqrt(d), dV = P^T dO summed over the G sharing query heads
+    (oracle.py:149-151)."""
+    q = np.asarray(q, np.float64)
+    k = np.asarray(k, np.float64)[:, keys]
+    v = np.asarray(v, np.float64)[:, keys]
+    do = np.asarray(d_out, np.float64)
+    n_q, n_kv = q.shape[0], k.shape[0]
+    g = _group(n_q, n_kv)
+    scale = 1.0 / math.sqrt(q.shape[-1])
+    s = _masked_scores(q, k, q_pos, np.asarray(k_pos)[keys], causal)
+    lse = np.asarray(lse, np.float64)
+    live = np.isfinite(lse)
+    p = np.exp(s - np.where(live, lse, 0.0)[..., None])
+    p = np.where(np.isneginf(s) | ~live[..., None], 0.0, p)
+    dp = np.matmul(do, np.repeat(v, g, axis=0).transpose(0, 2, 1))
+    ds = p * (dp - np.asarray(delta, np.float64)[..., None])
+    dk_r = np.matmul(ds.transpose(0, 2, 1), q) * scale
+    dv_r = np.matmul(p.transpose(0, 2, 1), do)
+    fold = (n_kv, g) + dk_r.shape[1:]
+    return dk_r.reshape(fold).sum(axis=1), dv_r.reshape(fold).sum(axis=1)
+
+
 def empty_block(heads, tokens, head_dim):
     return Block(np.zeros((heads, tokens, head_dim)),
                  np.full((heads, tokens), -np.inf))

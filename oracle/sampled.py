@@ -1,0 +1,196 @@
+"""Sampled parity at full problem size — TEST INFRASTRUCTURE ONLY.
+
+The dense oracle (``attn2d_oracle.attention`` / ``attention_grads``) needs the
+(H, S, S) score tensor: 275 GB at S=32K, 4.4 TB at S=128K. This module checks a
+GPU run at its real size on sampled rows and keys instead:
+
+* O, LSE, dQ on sampled query rows: ``attention_rows`` / ``attention_grads_rows``
+  (f64 numpy, exact — every quantity of a query row depends on that row alone,
+  ref ``test_oracle.py:79-85``).
+* dK, dV on sampled key columns: ``attention_key_grads`` (f64 numpy), which
+  needs every query row's LSE and delta = rowsum(dP*P) (ref ``oracle.py:145``).
+  Those two per-row statistics come from a blocked float64 pass over all rows
+  on the GPU (torch float64 matmuls; no bf16, no tensor-core shortcuts), and
+  that pass is itself pinned to the f64 CPU oracle on the sampled rows
+  (``pin_lse`` / ``pin_delta`` in the result, asserted <= 1e-9 by callers).
+
+Inputs are the bf16 values the kernels consumed, upcast exactly to f64, so the
+comparison isolates kernel error. Only ``tests/``, ``__graft_entry__.smoke()``
+and ``bench.py``'s check / CPU legs import this; the product never does.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import attn2d_oracle as orc
+
+
+def sample_indices(n: int, count: int, seed: int, stripes: int = 16) -> np.ndarray:
+    """Sorted unique indices: both ends, 64/128-tile boundaries near the ends,
+    every 1/`stripes` boundary (zig-zag stripe edges for d_cp <= stripes/2),
+    then uniform random fill up to `count`."""
+    fixed = {0, 1, 63, 64, 127, 128, 255, 256, n - 1, n - 2, n - 64, n - 65, n - 128, n - 129}
+    for s in range(1, stripes):
+        b = s * n // stripes
+        fixed.update((b - 1, b))
+    idx = sorted(i for i in fixed if 0 <= i < n)
+    rng = np.random.Generator(np.random.Philox(seed))
+    extra = max(0, count - len(idx))
+    if extra:
+        pool = np.setdiff1d(np.arange(n), idx)
+        idx = np.concatenate([idx, rng.choice(pool, size=min(extra, pool.size), replace=False)])
+    return np.unique(np.asarray(idx, np.int64))
+
+
+def row_stats_f64(qh, kh, vh, doh, qpos, kpos, causal: bool):
+    """Per-row (lse, delta) of one query head in float64 on the tensors' device.
+
+    qh/doh (Tq, d), kh/vh (Tk, d) torch float64; qpos/kpos int64 torch.
+    lse = natural-log logsumexp of the masked scaled scores (-inf for a row with
+    no admitted key), delta = rowsum(dO * O) with O = softmax * V."""
+    import torch
+
+    tq, tk = qh.shape[0], kh.shape[0]
+    d = qh.shape[1]
+    scale = 1.0 / math.sqrt(d)
+    lse = torch.empty(tq, dtype=torch.float64, device=qh.device)
+    delta = torch.empty(tq, dtype=torch.float64, device=qh.device)
+    ksorted = bool((kpos[1:] >= kpos[:-1]).all()) if tk > 1 else True
+    block = max(64, min(tq, (1 << 27) // max(tk, 1)))
+    for r0 in range(0, tq, block):
+        r1 = min(tq, r0 + block)
+        qp = qpos[r0:r1]
+        kl = tk
+        if causal and ksorted:
+            kl = int(torch.searchsorted(kpos, qp.max(), right=True))
+        if kl == 0:
+            lse[r0:r1] = -math.inf
+            delta[r0:r1] = 0.0
+            continue
+        s = (qh[r0:r1] @ kh[:kl].T) * scale
+        if causal:
+            s.masked_fill_(kpos[None, :kl] > qp[:, None], -math.inf)
+        m = s.amax(dim=1)
+        m0 = torch.where(torch.isinf(m), torch.zeros_like(m), m)
+        s.sub_(m0[:, None]).exp_()
+        z = s.sum(dim=1)
+        live = z > 0
+        zs = torch.where(live, z, torch.ones_like(z))
+        o = (s @ vh[:kl]) / zs[:, None]
+        lse[r0:r1] = torch.where(live, m0 + torch.log(zs), torch.full_like(z, -math.inf))
+        delta[r0:r1] = (doh[r0:r1] * o).sum(dim=1)
+        del s, o
+    return lse, delta
+
+
+BF16_ULP = 2.0 ** -8  # one bf16 ulp is at most 2^-7 |v| and at least 2^-8 |v|
+
+
+def _metrics(got, ref, bf16_out: bool):
+    """[max_abs, rel_l2, max|ref|, excess]: excess = max(|got - ref| - ulp_allow*|ref|)
+    with ulp_allow = 2^-8 for a bf16 output (the API's gradient/output dtype:
+    a bf16 value cannot be closer to the truth than its own rounding, about
+    |v|*2^-9, so for |ref| >~ 5 the absolute 2e-2 bar is below representation
+    error) and 0 for fp32 outputs (LSE)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    fin = np.isfinite(ref)
+    if not np.array_equal(np.isfinite(got), fin):
+        return [math.inf, math.inf, float(np.abs(ref[fin]).max()) if fin.any() else 0.0, math.inf]
+    if not fin.any():
+        return [0.0, 0.0, 0.0, 0.0]
+    dd = np.abs(got[fin] - ref[fin])
+    allow = BF16_ULP * np.abs(ref[fin]) if bf16_out else 0.0
+    return [float(dd.max()), float(np.linalg.norm(dd) / max(np.linalg.norm(ref[fin]), 1e-30)),
+            float(np.abs(ref[fin]).max()), float(max((dd - allow).max(), 0.0))]
+
+
+def _fold(acc, key, m):
+    """Worst-case merge of per-head metrics (max of max-abs, max of rel-L2)."""
+    if key not in acc:
+        acc[key] = list(m)
+    else:
+        acc[key] = [max(a, b) for a, b in zip(acc[key], m)]
+
+
+def check(q, k, v, do, out=None, dq=None, dk=None, dv=None, lse=None, *, causal=True, kv_heads=None,
+          n_rows=512, n_keys=256, seed=0, q_pos=None, k_pos=None):
+    """Compare a GPU run (global view, natural token order) with the oracle on
+    sampled rows/keys of the kv-head groups ``kv_heads`` (default: first and
+    last). q/do/out/dq (H, S, d), k/v/dk/dv (H_kv, S, d), lse (H, S) — torch
+    tensors on one device; any of the outputs may be None (not checked).
+    Returns {tensor: [max_abs, rel_l2, max|ref|, excess over one bf16 ulp], "pin_lse": .., "pin_delta": ..,
+    "rows": .., "keys": .., "heads": [...]}."""
+    import torch
+
+    H, S, d = q.shape
+    Hkv = k.shape[0]
+    G = H // Hkv
+    dev = q.device
+    if kv_heads is None:
+        kv_heads = sorted({0, Hkv - 1})
+    qpos = np.arange(S) if q_pos is None else np.asarray(q_pos, np.int64)
+    kpos = np.arange(k.shape[1]) if k_pos is None else np.asarray(k_pos, np.int64)
+    rows = sample_indices(S, n_rows, seed)
+    keys = sample_indices(k.shape[1], n_keys, seed + 1)
+    tq = torch.as_tensor(qpos, device=dev)
+    tk = torch.as_tensor(kpos, device=dev)
+    f64 = lambda x: x.to(torch.float64)  # noqa: E731 (exact bf16 -> f64)
+    b16 = lambda x: x.dtype == torch.bfloat16  # noqa: E731
+    cpu = lambda x: x.detach().to(torch.float64).cpu().numpy()  # noqa: E731
+    res: dict = {}
+    pin_lse = pin_delta = 0.0
+    heads = []
+    for hk in kv_heads:
+        hs = list(range(hk * G, (hk + 1) * G))
+        heads += hs
+        kh, vh = f64(k[hk]), f64(v[hk])
+        lse64 = np.empty((G, S))
+        delta64 = np.empty((G, S))
+        for i, h in enumerate(hs):
+            l, dl = row_stats_f64(f64(q[h]), kh, vh, f64(do[h]), tq, tk, causal)
+            lse64[i], delta64[i] = l.cpu().numpy(), dl.cpu().numpy()
+        del kh, vh
+        qg, kg, vg, dog = cpu(q[hs[0]:hs[-1] + 1]), cpu(k[hk:hk + 1]), cpu(v[hk:hk + 1]), cpu(do[hs[0]:hs[-1] + 1])
+        # ---- query rows: O, LSE, dQ (exact f64 oracle)
+        ro, rl = orc.attention_rows(qg, kg, vg, qpos, kpos, rows, causal)
+        rdq = orc.attention_grads_rows(qg, kg, vg, dog[:, rows], qpos, kpos, rows, causal)
+        fin = np.isfinite(rl)
+        pin_lse = max(pin_lse, float(np.abs(lse64[:, rows][fin] - rl[fin]).max()) if fin.any() else 0.0)
+        rdelta = (dog[:, rows] * ro).sum(axis=-1)
+        pin_delta = max(pin_delta, float(np.abs(delta64[:, rows] - rdelta).max()))
+        if out is not None:
+            _fold(res, "O", _metrics(cpu(out[hs[0]:hs[-1] + 1, rows]), ro, b16(out)))
+        if lse is not None:
+            _fold(res, "LSE", _metrics(cpu(lse[hs[0]:hs[-1] + 1, rows]), rl, b16(lse)))
+        if dq is not None:
+            _fold(res, "dQ", _metrics(cpu(dq[hs[0]:hs[-1] + 1, rows]), rdq, b16(dq)))
+        # ---- key columns: dK, dV given every row's f64 (lse, delta)
+        if dk is not None or dv is not None:
+            rdk, rdv = orc.attention_key_grads(qg, kg, vg, dog, qpos, kpos, keys, lse64, delta64, causal)
+            if dk is not None:
+                _fold(res, "dK", _metrics(cpu(dk[hk:hk + 1, keys]), rdk, b16(dk)))
+            if dv is not None:
+                _fold(res, "dV", _metrics(cpu(dv[hk:hk + 1, keys]), rdv, b16(dv)))
+    res.update({"pin_lse": pin_lse, "pin_delta": pin_delta, "rows": int(rows.size), "keys": int(keys.size),
+                "heads": heads})
+    return res
+
+
+def passes(res: dict, max_abs: float = 2e-2, rel_l2: float = 1e-2, pin: float = 1e-9) -> list[str]:
+    """Violations of the north-star bar per tensor: rel-L2 <= 1e-2 and
+    |got - ref| <= 2e-2 (+ one bf16 ulp of ref for bf16 outputs; equals the
+    plain absolute bar wherever |ref| is small — see _metrics)."""
+    bad = []
+    for name in ("O", "LSE", "dQ", "dK", "dV"):
+        if name in res:
+            ma, rl, _, ex = res[name]
+            if not (ex <= max_abs and rl <= rel_l2):
+                bad.append(f"{name}: max-abs {ma:.3e} (beyond one bf16 ulp {ex:.3e}) rel-L2 {rl:.3e}")
+    for name in ("pin_lse", "pin_delta"):
+        if not res[name] <= pin:
+            bad.append(f"{name} {res[name]:.3e} > {pin}")
+    return bad

@@ -37,8 +37,10 @@ SIGNATURES = {
     "a2d_nccl_unique_id": [_vp, _c_i64],
     "a2d_ctx_create": [_vp, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_i32,
                        _vp],
-    "a2d_fwd": [_vp, _vp, _vp, _vp, _vp, _vp],
-    "a2d_bwd": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "a2d_saved_bytes": [_vp, _vp],
+    "a2d_fwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "a2d_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "a2d_sync": [_vp, _vp, _c_i64],
     "a2d_ctx_destroy": [_vp],
     "a2d_ring_plan": [_c_i32, _c_i32, _c_i32, _vp, _vp],
     "a2d_zigzag_positions": [_c_i64, _c_i32, _c_i32, _vp],
@@ -67,8 +69,15 @@ def load(path: str = LIB_PATH):
     lib.a2d_last_error.restype = ctypes.c_char_p
     lib.a2d_last_error.argtypes = []
     lib.a2d_abi_version.restype = _c_int
+    lib.a2d_launch_count.restype = ctypes.c_longlong
+    lib.a2d_launch_count.argtypes = []
     _lib = lib
     return lib
+
+
+def launch_count() -> int:
+    """Kernels launched so far by the library in this process (C-side counter)."""
+    return int(load().a2d_launch_count())
 
 
 # kernels each entry point launches (for the bench's gpu_launches accounting)
@@ -86,7 +95,7 @@ class LaunchLog:
         self.count = 0
         self.by_name: dict[str, int] = {}
         self.timed: set[str] = set()
-        self.events: list = []  # (name, start_event, end_event)
+        self.events: list = []  # (name, start_event, end_event, algorithmic bytes moved)
 
     def reset(self, timed=()):
         self.count = 0
@@ -98,12 +107,16 @@ class LaunchLog:
 LOG = LaunchLog()
 
 
-def call(name: str, *args) -> None:
-    """Invoke an entry point; map non-zero status to ValueError / KernelError."""
+def call(name: str, *args, nbytes: int = 0, launches: int | None = None) -> None:
+    """Invoke an entry point; map non-zero status to ValueError / KernelError.
+
+    ``nbytes``: algorithmic HBM bytes the call moves (read + write of every
+    element, for the bench's HBM roofline); ``launches``: kernels it launches
+    when that depends on the arguments (default LAUNCHES[name])."""
     lib = load()
     ev = None
     if LOG.enabled:
-        LOG.count += LAUNCHES.get(name, 0)
+        LOG.count += LAUNCHES.get(name, 0) if launches is None else launches
         LOG.by_name[name] = LOG.by_name.get(name, 0) + 1
         if name in LOG.timed:
             import torch
@@ -112,9 +125,11 @@ def call(name: str, *args) -> None:
     rc = getattr(lib, name)(*args)
     if ev is not None:
         ev[1].record()
-        LOG.events.append((name, ev[0], ev[1]))
+        LOG.events.append((name, ev[0], ev[1], nbytes))
     if rc != 0:
         msg = lib.a2d_last_error().decode()
         if rc == 1:
             raise ValueError(msg)
+        if rc == 3:
+            raise TimeoutError(msg)
         raise KernelError(msg)

@@ -34,6 +34,19 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found (CUDA 12.9 toolkit required)")
 
 
+def nccl_dirs() -> tuple[str, str]:
+    """(include, lib) of the NCCL torch loads (2.28.x from the nvidia-nccl wheel):
+    the library links and rpaths it, so whichever of torch / this library is
+    loaded first, one NCCL ends up in the process (the system 2.27 would shadow
+    symbols torch needs)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia.nccl (torch's NCCL wheel) not found")
+    base = list(spec.submodule_search_locations)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
 def _deps() -> list[str]:
     out = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     out.append(os.path.join(ROOT, "include", "attn2d_sm100.h"))
@@ -53,12 +66,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     cc = nvcc()
+    nccl_inc, nccl_lib = nccl_dirs()
     procs = []
     objs = []
     for src in SOURCES:
         obj = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [cc, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        cmd = [cc, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-c",
                os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     failed = []
@@ -75,7 +89,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         msg = "\n".join(f"--- {s}\n{o[-6000:]}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = LIB + ".tmp"
-    cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC", "-lnccl"]
+    cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC", "-L", nccl_lib, "-l:libnccl.so.2",
+           "-Xlinker", f"-rpath={nccl_lib}"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}")

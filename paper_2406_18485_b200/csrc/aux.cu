@@ -52,53 +52,105 @@ cudaError_t launch_tile_bounds(const int* pos, int T, int tile, int2* out, cudaS
   return cudaGetLastError();
 }
 
-// One warp per query row; D = 128 or 64 bf16 elements.
+// delta / lse2 per query row. D/8 lanes per row, one 128-bit load of dO and
+// of O per lane (D = 128: 2 rows per warp, each warp load a 512-byte run);
+// the row sum is a shuffle reduction inside the lane group.
+template <int D>
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                       int64_t o_sh, int64_t o_st, int64_t do_sh, int64_t do_st,
-                                      const float* __restrict__ lse, int H, int Tq, int Tq_pad, int D,
+                                      const float* __restrict__ lse, int H, int Tq, int Tq_pad,
                                       float* __restrict__ lse2, float* __restrict__ delta) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x & 31;
-  if (warp >= H * Tq_pad) return;
-  const int h = warp / Tq_pad, t = warp % Tq_pad;
-  float acc = 0.f;
-  if (t < Tq) {
-    const __nv_bfloat16* po = o + h * o_sh + t * o_st;
-    const __nv_bfloat16* pd = dout + h * do_sh + t * do_st;
-    for (int c = lane * 2; c < D; c += 64) {
-      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(po + c));
-      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(pd + c));
-      acc += a.x * b.x + a.y * b.y;
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) {
-    float l2 = INFINITY;
+  constexpr int kLanes = D / 8;  // lanes per row
+  const int64_t rows = (int64_t)H * Tq_pad;
+  const int sub = threadIdx.x % kLanes;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kLanes; row < rows;
+       row += (int64_t)gridDim.x * blockDim.x / kLanes) {
+    const int h = (int)(row / Tq_pad), t = (int)(row % Tq_pad);
+    float acc = 0.f;
     if (t < Tq) {
-      const float l = lse[(size_t)h * Tq + t];
-      l2 = l == -INFINITY ? INFINITY : l * 1.4426950408889634f;
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + h * o_sh + t * o_st) + sub);
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(dout + h * do_sh + t * do_st) + sub);
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 x = __bfloat1622float2(pa[i]), y = __bfloat1622float2(pb[i]);
+        acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+      }
     }
-    lse2[(size_t)h * Tq_pad + t] = l2;
-    delta[(size_t)h * Tq_pad + t] = t < Tq ? acc : 0.f;
+#pragma unroll
+    for (int off = kLanes / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (sub == 0) {
+      float l2 = INFINITY;
+      if (t < Tq) {
+        const float l = lse[(size_t)h * Tq + t];
+        l2 = l == -INFINITY ? INFINITY : l * 1.4426950408889634f;
+      }
+      lse2[row] = l2;
+      delta[row] = t < Tq ? acc : 0.f;
+    }
   }
 }
 
 cudaError_t launch_bwd_preprocess(const __nv_bfloat16* o, const __nv_bfloat16* dout, int64_t o_sh, int64_t o_st,
                                   int64_t do_sh, int64_t do_st, const float* lse, int H, int Tq, int Tq_pad,
                                   int D, float* lse2, float* delta, cudaStream_t s) {
-  const int64_t warps = (int64_t)H * Tq_pad;
-  if (warps == 0) return cudaSuccess;
+  const int64_t rows = (int64_t)H * Tq_pad;
+  if (rows == 0) return cudaSuccess;
+  if ((o_st | do_st | o_sh | do_sh) % 8 || ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(dout)) & 15))
+    return cudaErrorInvalidValue;
   const int threads = 256;
-  const int64_t blocks = (warps * 32 + threads - 1) / threads;
-  bwd_preprocess_kernel<<<(unsigned)blocks, threads, 0, s>>>(o, dout, o_sh, o_st, do_sh, do_st, lse, H, Tq,
-                                                             Tq_pad, D, lse2, delta);
+  const int lanes = D / 8;
+  int64_t blocks = (rows * lanes + threads - 1) / threads;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (blocks > (int64_t)n_sm * 16) blocks = (int64_t)n_sm * 16;
+  if (D == 128) {
+    bwd_preprocess_kernel<128><<<(unsigned)blocks, threads, 0, s>>>(o, dout, o_sh, o_st, do_sh, do_st, lse, H, Tq,
+                                                                     Tq_pad, lse2, delta);
+  } else if (D == 64) {
+    bwd_preprocess_kernel<64><<<(unsigned)blocks, threads, 0, s>>>(o, dout, o_sh, o_st, do_sh, do_st, lse, H, Tq,
+                                                                    Tq_pad, lse2, delta);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
-// acc := block_update(acc, blk). acc_o fp32 [R][D]; blk_o bf16 or fp32.
-template <typename TB>
-__global__ void merge_kernel(float* __restrict__ acc_o, float* __restrict__ acc_lse, const TB* __restrict__ blk_o,
-                             const float* __restrict__ blk_lse, int64_t rows, int D) {
+// acc := block_update(acc, blk) (oracle.py:111-124). acc_o / blk_o fp32
+// [R][D], D % 4 == 0: one warp per row, 128-bit loads and stores (D = 128: one
+// float4 per lane, 512 contiguous bytes per warp access).
+__global__ void merge_kernel(float4* __restrict__ acc_o, float* __restrict__ acc_lse, const float4* __restrict__ blk_o,
+                             const float* __restrict__ blk_lse, int64_t rows, int d4) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < rows; r += warps) {
+    const float la = acc_lse[r], lb = blk_lse[r];
+    const float m = fmaxf(la, lb);
+    float wa = 0.f, wb = 0.f, ln = -INFINITY;
+    if (m != -INFINITY) {
+      const float ea = la == -INFINITY ? 0.f : expf(la - m);
+      const float eb = lb == -INFINITY ? 0.f : expf(lb - m);
+      const float z = ea + eb;
+      ln = m + logf(z);
+      wa = ea / z;
+      wb = eb / z;
+    }
+    for (int c = lane; c < d4; c += 32) {
+      const int64_t i = r * d4 + c;
+      const float4 a = acc_o[i], b = __ldg(blk_o + i);
+      acc_o[i] = make_float4(a.x * wa + b.x * wb, a.y * wa + b.y * wb, a.z * wa + b.z * wb, a.w * wa + b.w * wb);
+    }
+    __syncwarp();  // every lane has read acc_lse[r]
+    if (lane == 0) acc_lse[r] = ln;
+  }
+}
+
+// any D / alignment (small head dims through the reference-shaped API)
+__global__ void merge_scalar_kernel(float* __restrict__ acc_o, float* __restrict__ acc_lse,
+                                    const float* __restrict__ blk_o, const float* __restrict__ blk_lse, int64_t rows,
+                                    int D) {
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -113,17 +165,22 @@ __global__ void merge_kernel(float* __restrict__ acc_o, float* __restrict__ acc_
     wa = ea / z;
     wb = eb / z;
   }
-  for (int c = lane; c < D; c += 32) {
-    const float b = static_cast<float>(blk_o[r * D + c]);
-    acc_o[r * D + c] = acc_o[r * D + c] * wa + b * wb;
-  }
+  for (int c = lane; c < D; c += 32) acc_o[r * D + c] = acc_o[r * D + c] * wa + blk_o[r * D + c] * wb;
+  __syncwarp();
   if (lane == 0) acc_lse[r] = ln;
 }
 
 cudaError_t launch_merge_f32(float* acc_o, float* acc_lse, const float* blk_o, const float* blk_lse, int64_t rows,
                              int D, cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
-  merge_kernel<float><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(acc_o, acc_lse, blk_o, blk_lse, rows, D);
+  if (D % 4 || ((reinterpret_cast<uintptr_t>(acc_o) | reinterpret_cast<uintptr_t>(blk_o)) & 15)) {
+    merge_scalar_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(acc_o, acc_lse, blk_o, blk_lse, rows, D);
+    return cudaGetLastError();
+  }
+  int64_t blocks = (rows + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  merge_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4*>(acc_o), acc_lse,
+                                                reinterpret_cast<const float4*>(blk_o), blk_lse, rows, D / 4);
   return cudaGetLastError();
 }
 
@@ -186,36 +243,46 @@ cudaError_t launch_permute_f32_bf16(const float* src, __nv_bfloat16* dst, int64_
 
 // dQ out of the backward's transposed accumulator: dst[a][h][l][d] =
 // bf16(src[h][d][a*L + l]), L = T/A (A = d_hp: the gradient all-to-all's pack;
-// A = 1: plain [h][t][d]). 32-token tiles through shared memory so both the
-// query-contiguous reads and the feature-contiguous writes coalesce.
-__global__ void dqt_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int H, int64_t T,
-                                   int64_t T_pad, int64_t L) {
-  __shared__ float tile[128][33];
+// A = 1: plain [h][t][d]). No shared memory: a block owns 128 tokens x all
+// 128 features of one head; warp w reads features 8w..8w+7 as float4 runs
+// along the tokens (each warp load = 512 contiguous bytes), transposes the
+// 8x4 register block and writes four 16-byte rows of 8 bf16 features. The 16
+// warps of a block together write every 256-byte token row, so the partial
+// lines merge in L2 before they reach DRAM.
+__global__ void __launch_bounds__(512) dqt_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                          int H, int64_t T, int64_t T_pad, int64_t L) {
   const int h = blockIdx.y;
-  const int64_t t0 = (int64_t)blockIdx.x * 32;
-  const float* s = src + (size_t)h * 128 * T_pad;
-  for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) {
-    const int d = i / 32, tt = i % 32;
-    tile[d][tt] = (t0 + tt < T) ? s[(size_t)d * T_pad + t0 + tt] : 0.f;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {  // (token, 4-feature chunk)
-    const int tt = i / 32, c = i % 32;
-    const int64_t t = t0 + tt;
-    if (t >= T) continue;
-    const int64_t a = t / L, l = t % L;
-    __nv_bfloat162 lo = __floats2bfloat162_rn(tile[4 * c][tt], tile[4 * c + 1][tt]);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(tile[4 * c + 2][tt], tile[4 * c + 3][tt]);
-    uint2 u = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-    *reinterpret_cast<uint2*>(dst + (((size_t)a * H + h) * L + l) * 128 + 4 * c) = u;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t t = (int64_t)blockIdx.x * 128 + 4 * lane;
+  if (t >= T) return;
+  const int f0 = 8 * w;
+  const float* s = src + ((size_t)h * 128 + f0) * T_pad + t;
+  float4 r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = __ldcs(reinterpret_cast<const float4*>(s + (size_t)i * T_pad));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t tok = t + j;
+    if (tok >= T) break;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = j == 0 ? r[i].x : j == 1 ? r[i].y : j == 2 ? r[i].z : r[i].w;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]), p3 = __floats2bfloat162_rn(v[6], v[7]);
+    const int64_t a = tok / L, l = tok % L;
+    *reinterpret_cast<uint4*>(dst + (((size_t)a * H + h) * L + l) * 128 + f0) =
+        make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                   *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
   }
 }
 
 cudaError_t launch_dqt_to_bf16(const float* src, __nv_bfloat16* dst, int H, int64_t T, int64_t T_pad, int A,
                                cudaStream_t s) {
   if (H == 0 || T == 0) return cudaSuccess;
-  dim3 grid((unsigned)((T + 31) / 32), H);
-  dqt_to_bf16_kernel<<<grid, 256, 0, s>>>(src, dst, H, T, T_pad, T / A);
+  if (T_pad % 4 || ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15))
+    return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((T + 127) / 128), H);
+  dqt_to_bf16_kernel<<<grid, 512, 0, s>>>(src, dst, H, T, T_pad, T / A);
   return cudaGetLastError();
 }
 

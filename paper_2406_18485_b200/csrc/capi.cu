@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -38,13 +39,17 @@ cudaError_t launch_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_
 
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};  // kernels launched through this library (a2d_launch_count)
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-static int cuda_status(cudaError_t e, const char* where) {
-  if (e == cudaSuccess) return A2D_OK;
+static int cuda_status(cudaError_t e, const char* where, int launches = 1) {
+  if (e == cudaSuccess) {
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
+    return A2D_OK;
+  }
   return fail(A2D_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
@@ -118,7 +123,8 @@ using namespace a2d;
 extern "C" {
 
 const char* a2d_last_error(void) { return g_err.c_str(); }
-int a2d_abi_version(void) { return 1; }
+int a2d_abi_version(void) { return 2; }
+long long a2d_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int a2d_tile_bounds(const int32_t* pos, int64_t T, int32_t tile, int32_t* out_minmax, void* stream) {
   if (T < 0 || tile <= 0 || T > INT32_MAX) return fail(A2D_EINVAL, "a2d_tile_bounds: bad T/tile");
@@ -251,6 +257,8 @@ int a2d_permute_blocks(const void* src, void* dst, int64_t A, int64_t B, int64_t
 int a2d_gather_blocks(const void* src, void* dst, const int32_t* map, const int32_t* dst_map, int64_t n,
                       int64_t block_bytes, void* stream) {
   if (n < 0 || block_bytes % 16 != 0) return fail(A2D_EINVAL, "a2d_gather_blocks: block_bytes % 16 != 0");
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(A2D_EINVAL, "a2d_gather_blocks: pointers must be 16-byte aligned");
   return cuda_status(launch_gather_blocks(src, dst, map, dst_map, n, block_bytes, sm_count(), S(stream)),
                      "a2d_gather_blocks");
 }

@@ -11,13 +11,18 @@
 // overlaps the attention kernel beside it. The compute is the library's own
 // chunk kernels (a2d_fa_fwd_chunk, a2d_fa_bwd_chunk, packs, conversions).
 // Scope: head dim 128, head-major [H][L][d] SeqSharded tensors in zig-zag
-// token order (layout.seq_positions); one forward in flight per context (its
-// state is kept for the matching a2d_bwd, and with d_hp = 1 the caller's q
-// must stay valid until then).
+// token order (layout.seq_positions). The forward's state (the HeadSharded Q,
+// K/V chunk, output and LSE the backward needs) lives in a CALLER-OWNED
+// buffer of a2d_saved_bytes() bytes, so any number of layers / micro-batches
+// can be in flight and the context holds no per-call state (the reference
+// operator is a pure function, ring.py:82-119). The context owns only
+// workspaces (ring buffers, staging), reused in stream order.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -51,18 +56,32 @@ struct Ctx {
   std::vector<int32_t*> pos, b128, b64;  // per CP chunk j (device)
   int32_t *smap = nullptr, *dmap_k = nullptr, *dmap_v = nullptr;
   std::vector<void*> allocs;
-  // buffers
-  uint16_t *kv_send = nullptr, *q_recv = nullptr, *kv_recv = nullptr, *qh_own = nullptr, *kvh = nullptr;
-  uint16_t *out_h = nullptr, *out_send = nullptr, *doh = nullptr, *g_send = nullptr, *dkv_send = nullptr;
+  // workspaces (no per-call state: see Saved)
+  uint16_t *kv_send = nullptr, *q_recv = nullptr, *kv_recv = nullptr;
+  uint16_t *doh = nullptr, *g_send = nullptr, *dkv_send = nullptr;
   uint16_t* ring[4] = {nullptr, nullptr, nullptr, nullptr};  // inner0, inner1, outer0, outer1
-  float *lse = nullptr, *acc = nullptr, *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr;
+  float *acc = nullptr, *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr;
   float *dkv = nullptr, *part = nullptr, *dacc[2] = {nullptr, nullptr}, *g32_send = nullptr, *g32_recv = nullptr;
   float* g32_sum = nullptr;
   void* dkv_home = nullptr;
-  const uint16_t* qh = nullptr;   // qh_own, or the caller's q when d_hp == 1
-  const uint16_t* dO = nullptr;   // doh, or the caller's dout when d_hp == 1
-  bool have_state = false;
+  size_t off_kv = 0, off_out = 0, off_lse = 0, saved_bytes = 0;  // Saved layout
 };
+
+// One forward's state inside the caller's saved buffer (256-byte aligned
+// regions): HeadSharded Q [Hl][C][128] bf16, K/V chunk [2][Hkl][C][128] bf16,
+// output [Hl][C][128] bf16, natural-log LSE [Hl][C] fp32.
+struct Saved {
+  uint16_t* qh;
+  uint16_t* kvh;
+  uint16_t* out_h;
+  float* lse;
+};
+
+Saved saved_view(const Ctx& c, const void* base) {
+  char* b = static_cast<char*>(const_cast<void*>(base));
+  return {reinterpret_cast<uint16_t*>(b), reinterpret_cast<uint16_t*>(b + c.off_kv),
+          reinterpret_cast<uint16_t*>(b + c.off_out), reinterpret_cast<float*>(b + c.off_lse)};
+}
 
 #define NCCL_TRY(x)                                                                                  \
   do {                                                                                               \
@@ -143,6 +162,14 @@ std::vector<int32_t> cp_positions(int64_t S, int d_cp, int j) {
   return out;
 }
 
+void abort_comms(Ctx& c) {
+  for (ncclComm_t* m : {&c.c_dkv, &c.c_outer, &c.c_inner, &c.hp_comm, &c.world_comm})
+    if (*m) {
+      ncclCommAbort(*m);
+      *m = nullptr;
+    }
+}
+
 int destroy(Ctx* c) {
   if (!c) return A2D_OK;
   cudaDeviceSynchronize();
@@ -175,13 +202,13 @@ int gather_f32_to_bf16(Ctx& c, const float* src, int B, uint16_t* dst, cudaStrea
   return a2a(c, c.g_send, dst, (size_t)B * c.L * 128 * 2, s);
 }
 
-int ring_forward(Ctx& c, cudaStream_t s) {
+int ring_forward(Ctx& c, const Saved& sv, cudaStream_t s) {
   const size_t kv_elems = (size_t)2 * c.Hkl * c.C * 128, kv_bytes = kv_elems * 2, half = kv_elems / 2;
   const int64_t q_rows = (int64_t)c.C;
   if (c.d_cp == 1)
-    return a2d_fa_fwd_chunk(c.qh, c.kvh, c.kvh + half, c.pos[c.cp], c.pos[c.cp], c.b128[c.cp], c.b128[c.cp], c.Hl, c.Hkl,
-                            q_rows, q_rows, 128, c.causal, c.scale, 0, c.lse, nullptr, c.out_h, s);
-  const uint16_t *cur = c.kvh, *first = c.kvh;
+    return a2d_fa_fwd_chunk(sv.qh, sv.kvh, sv.kvh + half, c.pos[c.cp], c.pos[c.cp], c.b128[c.cp], c.b128[c.cp], c.Hl,
+                            c.Hkl, q_rows, q_rows, 128, c.causal, c.scale, 0, sv.lse, nullptr, sv.out_h, s);
+  const uint16_t *cur = sv.kvh, *first = sv.kvh;
   uint16_t* nxt_inner = nullptr;
   uint16_t* nxt_outer = nullptr;
   int n_out = 0;
@@ -198,9 +225,9 @@ int ring_forward(Ctx& c, cudaStream_t s) {
       nxt_inner = c.ring[(t + 1) % 2];
       A2D_TRY(hop(c, c.c_inner, c.s_inner, s, cur, c.inner_to, nxt_inner, c.inner_from, kv_bytes, c.ev_inner));
     }
-    A2D_TRY(a2d_fa_fwd_chunk(c.qh, cur, cur + half, c.pos[c.cp], c.pos[step.source], c.b128[c.cp],
+    A2D_TRY(a2d_fa_fwd_chunk(sv.qh, cur, cur + half, c.pos[c.cp], c.pos[step.source], c.b128[c.cp],
                              c.b128[step.source], c.Hl, c.Hkl, q_rows, q_rows, 128, c.causal, c.scale, st > 0 ? 1 : 0,
-                             c.lse, c.acc, last ? c.out_h : nullptr, s));
+                             sv.lse, c.acc, last ? sv.out_h : nullptr, s));
     if (t + 1 < c.w) {
       CUDA_TRY(cudaStreamWaitEvent(s, c.ev_inner, 0));
       cur = nxt_inner;
@@ -213,12 +240,12 @@ int ring_forward(Ctx& c, cudaStream_t s) {
 }
 
 // returns the home dK/dV buffer ([2][Hkl][C][128]) and whether it is bf16
-int ring_backward(Ctx& c, cudaStream_t s, const void** home, bool* home_bf16) {
+int ring_backward(Ctx& c, const Saved& sv, const uint16_t* dO, cudaStream_t s, const void** home, bool* home_bf16) {
   const size_t kv_elems = (size_t)2 * c.Hkl * c.C * 128, kv_bytes = kv_elems * 2, half = kv_elems / 2;
   const int64_t T = (int64_t)c.C;
-  const uint16_t* kv_own = c.kvh;
+  const uint16_t* kv_own = sv.kvh;
   if (c.d_cp == 1) {
-    A2D_TRY(a2d_fa_bwd_chunk(c.qh, kv_own, kv_own + half, c.dO, c.pos[c.cp], c.pos[c.cp], c.b64[c.cp], c.b128[c.cp],
+    A2D_TRY(a2d_fa_bwd_chunk(sv.qh, kv_own, kv_own + half, dO, c.pos[c.cp], c.pos[c.cp], c.b64[c.cp], c.b128[c.cp],
                              c.lse2, c.delta, c.dq_acc, c.dkv, c.dkv + half, 0, c.Hl, c.Hkl, T, T, 128, c.causal,
                              c.scale, s));
     *home = c.dkv;
@@ -243,7 +270,7 @@ int ring_backward(Ctx& c, cudaStream_t s, const void** home, bool* home_bf16) {
       A2D_TRY(hop(c, c.c_inner, c.s_inner, s, cur, c.inner_to, nxt_inner, c.inner_from, kv_bytes, c.ev_inner));
     }
     float* tgt = st == 0 ? c.dacc[0] : c.part;
-    A2D_TRY(a2d_fa_bwd_chunk(c.qh, cur, cur + half, c.dO, c.pos[c.cp], c.pos[step.source], c.b64[c.cp],
+    A2D_TRY(a2d_fa_bwd_chunk(sv.qh, cur, cur + half, dO, c.pos[c.cp], c.pos[step.source], c.b64[c.cp],
                              c.b128[step.source], c.lse2, c.delta, c.dq_acc, tgt, tgt + half, 0, c.Hl, c.Hkl, T, T, 128,
                              c.causal, c.scale, s));
     if (st > 0) {  // the travelling accumulator of this chunk arrived in dacc[st % 2]
@@ -343,17 +370,18 @@ int create(const void* id, int rank, int world, int d_hp, int d_cp, int w, int p
   CUDA_TRY(cudaMemcpy(c->dmap_v, dv.data(), dv.size() * 4, cudaMemcpyHostToDevice));
   // ---- buffers
   const size_t qe = (size_t)c->Hl * C * 128, kve = (size_t)2 * c->Hkl * C * 128;
-  A2D_TRY(dalloc(*c, &c->kvh, kve));
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  c->off_kv = up(qe * 2);
+  c->off_out = c->off_kv + up(kve * 2);
+  c->off_lse = c->off_out + up(qe * 2);
+  c->saved_bytes = c->off_lse + up((size_t)c->Hl * C * 4);
   if (d_hp > 1) {
     A2D_TRY(dalloc(*c, &c->kv_send, kve));
     A2D_TRY(dalloc(*c, &c->q_recv, qe));
     A2D_TRY(dalloc(*c, &c->kv_recv, kve));
-    A2D_TRY(dalloc(*c, &c->qh_own, qe));
     A2D_TRY(dalloc(*c, &c->g_send, std::max(qe, kve / 2)));
+    A2D_TRY(dalloc(*c, &c->doh, qe));
   }
-  A2D_TRY(dalloc(*c, &c->out_h, qe));
-  if (d_hp > 1) A2D_TRY(dalloc(*c, &c->doh, qe));
-  A2D_TRY(dalloc(*c, &c->lse, (size_t)c->Hl * C));
   A2D_TRY(dalloc(*c, &c->lse2, (size_t)c->Hl * c->C_pad));
   A2D_TRY(dalloc(*c, &c->delta, (size_t)c->Hl * c->C_pad));
   A2D_TRY(dalloc(*c, &c->dq_acc, (size_t)c->Hl * 128 * c->C_pad));
@@ -379,43 +407,41 @@ int create(const void* id, int rank, int world, int d_hp, int d_cp, int w, int p
   return A2D_OK;
 }
 
-int forward(Ctx& c, const void* q, const void* k, const void* v, void* out, cudaStream_t s) {
+int forward(Ctx& c, const void* q, const void* k, const void* v, void* out, void* saved, cudaStream_t s) {
   const size_t L128 = (size_t)c.L * 128;
-  // KV pack [peer][2][Hkl][L][128] (GQA replication by the head map), q needs none
-  // (d_hp = 1: the pack IS the HeadSharded KV chunk)
-  uint16_t* kvp = c.d_hp == 1 ? c.kvh : c.kv_send;
+  const Saved sv = saved_view(c, saved);
+  // KV pack [peer][2][Hkl][L][128] (GQA replication by the head map); with
+  // d_hp = 1 the pack IS the HeadSharded KV chunk (written into the state)
+  uint16_t* kvp = c.d_hp == 1 ? sv.kvh : c.kv_send;
   A2D_TRY(a2d_gather_blocks(k, kvp, c.smap, c.dmap_k, (int64_t)c.d_hp * c.Hkl, (int64_t)L128 * 2, s));
   A2D_TRY(a2d_gather_blocks(v, kvp, c.smap, c.dmap_v, (int64_t)c.d_hp * c.Hkl, (int64_t)L128 * 2, s));
   if (c.d_hp == 1) {
-    c.qh = static_cast<const uint16_t*>(q);
+    // the state owns its Q (no aliasing of the caller's buffer)
+    CUDA_TRY(cudaMemcpyAsync(sv.qh, q, (size_t)c.Hl * L128 * 2, cudaMemcpyDeviceToDevice, s));
   } else {
     A2D_TRY(a2a(c, q, c.q_recv, (size_t)c.Hl * L128 * 2, s));
     A2D_TRY(a2a(c, c.kv_send, c.kv_recv, (size_t)2 * c.Hkl * L128 * 2, s));
-    A2D_TRY(a2d_permute_blocks(c.q_recv, c.qh_own, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
-    A2D_TRY(a2d_permute_blocks(c.kv_recv, c.kvh, c.d_hp, 2 * c.Hkl, (int64_t)L128 * 2, s));
-    c.qh = c.qh_own;
+    A2D_TRY(a2d_permute_blocks(c.q_recv, sv.qh, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
+    A2D_TRY(a2d_permute_blocks(c.kv_recv, sv.kvh, c.d_hp, 2 * c.Hkl, (int64_t)L128 * 2, s));
   }
-  A2D_TRY(ring_forward(c, s));
-  A2D_TRY(gather_bf16(c, c.out_h, c.Hl, static_cast<uint16_t*>(out), s));
-  c.have_state = true;
-  return A2D_OK;
+  A2D_TRY(ring_forward(c, sv, s));
+  return gather_bf16(c, sv.out_h, c.Hl, static_cast<uint16_t*>(out), s);
 }
 
-int backward(Ctx& c, const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
-  if (!c.have_state) return set_error(A2D_EINVAL, "a2d_bwd called before a2d_fwd");
+int backward(Ctx& c, const void* saved, const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
   const size_t L128 = (size_t)c.L * 128;
-  if (c.d_hp == 1) {
-    c.dO = static_cast<const uint16_t*>(dout);
-  } else {
+  const Saved sv = saved_view(c, saved);
+  const uint16_t* dO = static_cast<const uint16_t*>(dout);
+  if (c.d_hp > 1) {
     A2D_TRY(a2a(c, dout, c.q_recv, (size_t)c.Hl * L128 * 2, s));
     A2D_TRY(a2d_permute_blocks(c.q_recv, c.doh, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
-    c.dO = c.doh;
+    dO = c.doh;
   }
-  A2D_TRY(a2d_bwd_preprocess(c.out_h, c.dO, c.lse, c.Hl, c.C, 128, c.lse2, c.delta, s));
+  A2D_TRY(a2d_bwd_preprocess(sv.out_h, dO, sv.lse, c.Hl, c.C, 128, c.lse2, c.delta, s));
   CUDA_TRY(cudaMemsetAsync(c.dq_acc, 0, (size_t)c.Hl * 128 * c.C_pad * 4, s));
   const void* home = nullptr;
   bool home_bf16 = false;
-  A2D_TRY(ring_backward(c, s, &home, &home_bf16));
+  A2D_TRY(ring_backward(c, sv, dO, s, &home, &home_bf16));
   // dQ: transposed accumulator -> bf16 peer-major pack -> all-to-all into the caller's dq
   if (c.d_hp == 1) {
     A2D_TRY(a2d_dqt_to_bf16(c.dq_acc, dq, c.Hl, c.C, c.C_pad, 1, s));
@@ -441,6 +467,34 @@ int backward(Ctx& c, const void* dout, void* dq, void* dk, void* dv, cudaStream_
     }
   }
   return A2D_OK;
+}
+
+// Wait for `stream` while polling every communicator for an asynchronous NCCL
+// error; on an error or after timeout_ms, abort the communicators (so no rank
+// hangs forever on a dead peer) and report.
+int sync_checked(Ctx& c, cudaStream_t s, int64_t timeout_ms) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return A2D_OK;
+    if (q != cudaErrorNotReady) return set_error(A2D_ECUDA, std::string("a2d_sync: ") + cudaGetErrorString(q));
+    for (ncclComm_t m : {c.world_comm, c.hp_comm, c.c_inner, c.c_outer, c.c_dkv}) {
+      if (!m) continue;
+      ncclResult_t r = ncclSuccess;
+      if (ncclCommGetAsyncError(m, &r) != ncclSuccess || (r != ncclSuccess && r != ncclInProgress)) {
+        abort_comms(c);
+        return set_error(A2D_ECUDA, std::string("a2d_sync: NCCL asynchronous error: ") + ncclGetErrorString(r) +
+                                        " (communicators aborted)");
+      }
+    }
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms >= 0 && ms > timeout_ms) {
+      abort_comms(c);
+      return set_error(A2D_ETIMEOUT, "a2d_sync: timed out after " + std::to_string(ms) +
+                                         " ms (communicators aborted; the context is no longer usable)");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
 }
 
 }  // namespace
@@ -469,14 +523,33 @@ int a2d_ctx_create(const void* nccl_id, int32_t rank, int32_t world, int32_t d_h
   return A2D_OK;
 }
 
-int a2d_fwd(void* ctx, const void* q, const void* k, const void* v, void* out, void* stream) {
-  if (!ctx) return set_error(A2D_EINVAL, "a2d_fwd: null context");
-  return forward(*static_cast<Ctx*>(ctx), q, k, v, out, static_cast<cudaStream_t>(stream));
+int a2d_saved_bytes(void* ctx, int64_t* bytes) {
+  if (!ctx || !bytes) return set_error(A2D_EINVAL, "a2d_saved_bytes: null argument");
+  *bytes = (int64_t)static_cast<Ctx*>(ctx)->saved_bytes;
+  return A2D_OK;
 }
 
-int a2d_bwd(void* ctx, const void* dout, void* dq, void* dk, void* dv, void* stream) {
+int a2d_fwd(void* ctx, const void* q, const void* k, const void* v, void* out, void* saved, void* stream) {
+  if (!ctx) return set_error(A2D_EINVAL, "a2d_fwd: null context");
+  if (!saved || (reinterpret_cast<uintptr_t>(saved) & 255))
+    return set_error(A2D_EINVAL, "a2d_fwd: saved must be a 256-byte aligned buffer of a2d_saved_bytes() bytes");
+  Ctx& c = *static_cast<Ctx*>(ctx);
+  if (!c.world_comm) return set_error(A2D_EINVAL, "a2d_fwd: context was aborted");
+  return forward(c, q, k, v, out, saved, static_cast<cudaStream_t>(stream));
+}
+
+int a2d_bwd(void* ctx, const void* saved, const void* dout, void* dq, void* dk, void* dv, void* stream) {
   if (!ctx) return set_error(A2D_EINVAL, "a2d_bwd: null context");
-  return backward(*static_cast<Ctx*>(ctx), dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+  if (!saved || (reinterpret_cast<uintptr_t>(saved) & 255))
+    return set_error(A2D_EINVAL, "a2d_bwd: saved must be the buffer a2d_fwd filled");
+  Ctx& c = *static_cast<Ctx*>(ctx);
+  if (!c.world_comm) return set_error(A2D_EINVAL, "a2d_bwd: context was aborted");
+  return backward(c, saved, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+}
+
+int a2d_sync(void* ctx, void* stream, int64_t timeout_ms) {
+  if (!ctx) return set_error(A2D_EINVAL, "a2d_sync: null context");
+  return sync_checked(*static_cast<Ctx*>(ctx), static_cast<cudaStream_t>(stream), timeout_ms);
 }
 
 int a2d_ctx_destroy(void* ctx) { return destroy(static_cast<Ctx*>(ctx)); }

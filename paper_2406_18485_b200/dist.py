@@ -65,6 +65,54 @@ class StepTimes:
         self.events.clear()
 
 
+def make_groups(grid, group=None):
+    """(hp_group, (ring_inner, ring_outer, ring_dkv), replica_ranks) of this rank.
+
+    ``group`` (default WORLD) is this rank's replica: d_hp*d_cp ranks running
+    one 2D-attention layer; several data-parallel replicas may run side by
+    side. torch needs every WORLD rank to call new_group for every group, with
+    the same ranks, in the same order — so the replicas' rank lists are
+    gathered first and every rank creates the HP and ring groups of EVERY
+    replica in one global order (sorted replicas, then HP groups by cp, then
+    ring groups by hp)."""
+    world = dist.get_world_size()
+    if group is None:
+        mine = list(range(world))
+        replicas = [tuple(mine)]
+    else:
+        mine = dist.get_process_group_ranks(group)
+        allr = [None] * world
+        dist.all_gather_object(allr, list(mine))
+        replicas = sorted({tuple(r) for r in allr})
+        flat = sorted(r for rep in replicas for r in rep)
+        if flat != list(range(world)) or any(len(rep) != grid.d_sp for rep in replicas):
+            raise ValueError("replica groups must partition WORLD into groups of d_hp*d_cp ranks")
+    me = dist.get_rank()
+    hp_i, cp_j = grid.coords_of(mine.index(me))
+    hp_group, ring = None, (None, None, None)
+    for rep in replicas:
+        own = list(rep) == list(mine)
+        for j in range(grid.d_cp):
+            g = dist.new_group([rep[r] for r in grid.hp_group(j)]) if grid.d_hp > 1 else None
+            if own and j == cp_j:
+                hp_group = g
+        for i in range(grid.d_hp):
+            ranks = [rep[r] for r in grid.cp_group(i)]
+            gs = tuple(dist.new_group(ranks) if grid.d_cp > 1 else None for _ in range(3))
+            if own and i == hp_i:
+                ring = gs
+    return hp_group, ring, list(mine)
+
+
+class _State(tuple):
+    """(qh, kvh, out_h, lse) of one forward. ``guard`` = (tensor, version) when
+    qh aliases the caller's q (d_hp = 1, head-major bf16 input): the backward
+    refuses to run if q was modified in place in between (it would silently
+    produce wrong gradients otherwise)."""
+
+    guard = None
+
+
 class Attn2D:
     """Per-rank 2D-Attention operator (HP all-to-all x Double-Ring CP).
 
@@ -103,23 +151,7 @@ class Attn2D:
         self.C_pad = (self.C + 63) // 64 * 64
 
         # ---- process groups (created by every rank, in the same order)
-        self.hp_group = None
-        self.ring_inner = self.ring_outer = self.ring_dkv = None
-        base = group  # None = WORLD
-        g_ranks = list(range(self.world)) if base is None else dist.get_process_group_ranks(base)
-        for j in range(d_cp):
-            ranks = [g_ranks[r] for r in self.grid.hp_group(j)]
-            g = dist.new_group(ranks) if d_hp > 1 else None
-            if j == self.cp:
-                self.hp_group = g
-        for i in range(d_hp):
-            ranks = [g_ranks[r] for r in self.grid.cp_group(i)]
-            gi = dist.new_group(ranks) if d_cp > 1 else None
-            go = dist.new_group(ranks) if d_cp > 1 else None
-            gd = dist.new_group(ranks) if d_cp > 1 else None
-            if i == self.hp:
-                self.ring_inner, self.ring_outer, self.ring_dkv = gi, go, gd
-        self._g = g_ranks
+        self.hp_group, (self.ring_inner, self.ring_outer, self.ring_dkv), self._g = make_groups(self.grid, group)
 
         # ---- schedule and peers (global ranks)
         self.schedule = build_ring_schedule(d_cp, w)
@@ -192,10 +224,16 @@ class Attn2D:
         d_hp, tok = self.par.d_hp, self.L * self.bd
         self._in_bytes = d_hp * tok * 2 * (self.Hl + 2 * self.Hkl)
         out_bytes = d_hp * tok * (2 * self.Hl + 4 * 2 * self.Hkl)
+        ok = True
         try:  # e.g. an HP group spanning nodes cannot map peer memory: keep NCCL
             buf = symm.empty(self._in_bytes + out_bytes, dtype=torch.uint8, device=self.device)
             self._symm = symm.rendezvous(buf, self.hp_group.group_name)
-        except RuntimeError:
+        except Exception:  # noqa: BLE001 - any failure means "no symmetric memory here"
+            ok = False
+        # every HP rank must pick the same transport, or the group deadlocks
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.hp_group)
+        if not ok or int(flag.item()) == 0:
             self._symm = None
             return
         self._symm_buf = buf
@@ -675,7 +713,10 @@ class Attn2D:
         self._ring_forward(qh, kvh, out_h, lse)
         out = self._gather(out_h, "out", fresh=not tm)
         self._mark("fwd.a2a_out")
-        return self._to_layout(out, tm), (qh, kvh.unsqueeze(0), out_h, lse)
+        state = _State((qh, kvh.unsqueeze(0), out_h, lse))
+        if qh.data_ptr() == q.data_ptr():
+            state.guard = (q, q._version)
+        return self._to_layout(out, tm), state
 
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: str = "hld") -> torch.Tensor:
         """This rank's SeqSharded chunk -> SeqSharded output, bf16.
@@ -697,6 +738,10 @@ class Attn2D:
         if state is None:
             raise RuntimeError("backward called before forward")
         qh, kvh, out_h, lse = state
+        guard = getattr(state, "guard", None)
+        if guard is not None and guard[0]._version != guard[1]:
+            raise RuntimeError("q was modified in place between forward and backward (the saved state aliases it "
+                               "when d_hp = 1); clone q before modifying it")
         self._mark("bwd.start")
         bd = self.bd
         if self.ng > 1:

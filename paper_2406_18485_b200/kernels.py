@@ -16,6 +16,7 @@ from . import _lib
 BF16 = torch.bfloat16
 FWD_DIMS = (64, 128)
 BWD_DIM = 128
+BWD_QSLICE = 4096 * 64  # query rows per fa_bwd launch (capi.cu a2d_fa_bwd_chunk)
 
 
 def _stream() -> int:
@@ -96,7 +97,7 @@ def bwd_preprocess(o: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor):
     lse2 = torch.empty((H, tp), dtype=torch.float32, device=o.device)
     delta = torch.empty((H, tp), dtype=torch.float32, device=o.device)
     _lib.call("a2d_bwd_preprocess", o.data_ptr(), dout.data_ptr(), lse.data_ptr(), H, Tq, D,
-              lse2.data_ptr(), delta.data_ptr(), _stream())
+              lse2.data_ptr(), delta.data_ptr(), _stream(), nbytes=H * Tq * (4 * D + 4) + H * tp * 8)
     return lse2, delta
 
 
@@ -115,7 +116,8 @@ def dqt_to_bf16(acc: torch.Tensor, T: int, A: int = 1, out: torch.Tensor | None 
     H = acc.shape[0]
     if out is None:
         out = torch.empty((A, H, T // A, BWD_DIM), dtype=BF16, device=acc.device)
-    _lib.call("a2d_dqt_to_bf16", acc.data_ptr(), out.data_ptr(), H, T, acc.shape[2], A, _stream())
+    _lib.call("a2d_dqt_to_bf16", acc.data_ptr(), out.data_ptr(), H, T, acc.shape[2], A, _stream(),
+              nbytes=H * T * BWD_DIM * 6)
     return out
 
 
@@ -125,6 +127,7 @@ def bwd_chunk(q, k, v, dout, qp: ChunkPlan, kp: ChunkPlan, lse2, delta, dq_acc, 
     dq_acc fp32 TRANSPOSED [H][128][round_up(Tq, 64)] (see dq_acc_t / dqt_to_bf16)."""
     H, Tq, D = q.shape
     Hkv, Tk, _ = k.shape
+    n_launch = max(1, -(-Tq // BWD_QSLICE)) if Tk > 0 else 0  # the C ABI slices long query chunks
     if D != BWD_DIM:
         raise ValueError("backward kernel head dim must be 128")
     if dq_acc.shape != (H, BWD_DIM, (Tq + 63) // 64 * 64) or dq_acc.dtype != torch.float32:
@@ -132,15 +135,16 @@ def bwd_chunk(q, k, v, dout, qp: ChunkPlan, kp: ChunkPlan, lse2, delta, dq_acc, 
     _lib.call("a2d_fa_bwd_chunk", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
               qp.pos.data_ptr(), kp.pos.data_ptr(), qp.b64.data_ptr(), kp.b128.data_ptr(),
               lse2.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dk.data_ptr(), dv.data_ptr(),
-              int(accumulate_kv), H, Hkv, Tq, Tk, D, int(causal), float(scale), _stream())
+              int(accumulate_kv), H, Hkv, Tq, Tk, D, int(causal), float(scale), _stream(), launches=n_launch)
 
 
 def merge_(acc_o, acc_lse, blk_o, blk_lse) -> None:
     """In-place block_update of fp32 (acc_o, acc_lse) with (blk_o, blk_lse)."""
     d = acc_o.shape[-1]
     rows = acc_o.numel() // d
-    _lib.call("a2d_merge", acc_o.data_ptr(), acc_lse.data_ptr(), blk_o.contiguous().float().data_ptr()
-              if blk_o.dtype != torch.float32 else blk_o.data_ptr(), blk_lse.data_ptr(), rows, d, _stream())
+    blk = blk_o.contiguous().float()
+    _lib.call("a2d_merge", acc_o.data_ptr(), acc_lse.data_ptr(), blk.data_ptr(), blk_lse.data_ptr(), rows, d,
+              _stream(), nbytes=rows * (12 * d + 12))
 
 
 def permute_blocks(src: torch.Tensor, A: int, B: int, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -149,7 +153,7 @@ def permute_blocks(src: torch.Tensor, A: int, B: int, out: torch.Tensor | None =
     if out is None:
         out = torch.empty_like(src)
     blk = src.numel() * src.element_size() // max(A * B, 1)
-    _lib.call("a2d_permute_blocks", src.data_ptr(), out.data_ptr(), A, B, blk, _stream())
+    _lib.call("a2d_permute_blocks", src.data_ptr(), out.data_ptr(), A, B, blk, _stream(), nbytes=2 * A * B * blk)
     return out
 
 
@@ -162,7 +166,7 @@ def gather_blocks(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor,
     idx = index.to(device=src.device, dtype=torch.int32).contiguous()
     didx = None if dst_index is None else dst_index.to(device=src.device, dtype=torch.int32).contiguous()
     _lib.call("a2d_gather_blocks", src.data_ptr(), out.data_ptr(), idx.data_ptr(),
-              None if didx is None else didx.data_ptr(), idx.numel(), blk, _stream())
+              None if didx is None else didx.data_ptr(), idx.numel(), blk, _stream(), nbytes=2 * idx.numel() * blk)
     return out
 
 
@@ -184,7 +188,7 @@ def copy_rows(src: torch.Tensor, dst: torch.Tensor, src_map: torch.Tensor | None
     dm = None if dst_map is None else dst_map.to(device=dev, dtype=torch.int32).contiguous()
     _lib.call("a2d_copy_rows", src.data_ptr(), dst.data_ptr(), n_t, n_h, src.stride(0) * es, src.stride(1) * es,
               dst.stride(0) * es, dst.stride(1) * es, row, None if sm is None else sm.data_ptr(),
-              None if dm is None else dm.data_ptr(), _stream())
+              None if dm is None else dm.data_ptr(), _stream(), nbytes=2 * n_t * n_h * row)
     return dst
 
 
@@ -192,14 +196,15 @@ def sum_replicas(src: torch.Tensor, rep: int) -> torch.Tensor:
     """[H*rep, ...] fp32 -> [H, ...] summing consecutive copies."""
     heads = src.shape[0] // rep
     out = torch.empty((heads,) + tuple(src.shape[1:]), dtype=torch.float32, device=src.device)
-    _lib.call("a2d_sum_replicas_f32", src.data_ptr(), out.data_ptr(), heads, rep, src[0].numel(), _stream())
+    _lib.call("a2d_sum_replicas_f32", src.data_ptr(), out.data_ptr(), heads, rep, src[0].numel(), _stream(),
+              nbytes=4 * (rep + 1) * heads * src[0].numel())
     return out
 
 
 def to_bf16(src: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     if out is None:
         out = torch.empty(src.shape, dtype=BF16, device=src.device)
-    _lib.call("a2d_f32_to_bf16", src.data_ptr(), out.data_ptr(), src.numel(), _stream())
+    _lib.call("a2d_f32_to_bf16", src.data_ptr(), out.data_ptr(), src.numel(), _stream(), nbytes=6 * src.numel())
     return out
 
 
@@ -209,12 +214,13 @@ def permute_to_bf16(src: torch.Tensor, A: int, B: int, out: torch.Tensor | None 
     if out is None:
         out = torch.empty(src.shape, dtype=BF16, device=src.device)
     blk = src.numel() // max(A * B, 1)
-    _lib.call("a2d_permute_f32_to_bf16", src.data_ptr(), out.data_ptr(), A, B, blk, _stream())
+    _lib.call("a2d_permute_f32_to_bf16", src.data_ptr(), out.data_ptr(), A, B, blk, _stream(),
+              nbytes=6 * src.numel())
     return out
 
 
 def add_(dst: torch.Tensor, src: torch.Tensor) -> None:
-    _lib.call("a2d_add_f32", dst.data_ptr(), src.data_ptr(), dst.numel(), _stream())
+    _lib.call("a2d_add_f32", dst.data_ptr(), src.data_ptr(), dst.numel(), _stream(), nbytes=12 * dst.numel())
 
 
 def selftest_umma(a, b, v, at) -> torch.Tensor:

@@ -39,30 +39,59 @@ class NativeAttn2D:
                   par.inner_ring, placement, model.heads, model.kv_heads, model.head_dim, model.seq_len,
                   int(causal), ctypes.addressof(self._ctx))
         self.L = model.seq_len // self.world
-        self._q = None
+        nb = ctypes.c_int64()
+        _lib.call("a2d_saved_bytes", self._ctx, ctypes.addressof(nb))
+        self.saved_bytes = int(nb.value)
+        self.saved = None  # state of the last forward() (forward_with_state returns its own)
 
     def _empty(self, heads: int, like: torch.Tensor) -> torch.Tensor:
         return torch.empty((heads, self.L, self.model.head_dim), dtype=torch.bfloat16, device=like.device)
 
-    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+    def forward_with_state(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
+        """(out, state): state is a caller-owned device buffer holding this
+        call's HeadSharded Q, K/V, output and LSE, so any number of forwards
+        can be in flight before their backwards (stateless context)."""
         m = self.model
         for t, h in ((q, m.heads), (k, m.kv_heads), (v, m.kv_heads)):
             if tuple(t.shape) != (h, self.L, m.head_dim) or t.dtype != torch.bfloat16 or not t.is_contiguous():
                 raise ValueError(f"expected contiguous bf16 ({h}, {self.L}, {m.head_dim}), got {tuple(t.shape)}")
         out = self._empty(m.heads, q)
-        self._q = q  # with d_hp = 1 the runtime keeps reading q in the backward
-        _lib.call("a2d_fwd", self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+        state = torch.empty(self.saved_bytes, dtype=torch.uint8, device=q.device)  # caching allocator: 512-B aligned
+        _lib.call("a2d_fwd", self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), state.data_ptr(),
                   torch.cuda.current_stream().cuda_stream)
+        return out, state
+
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+        out, self.saved = self.forward_with_state(q, k, v)
         return out
 
-    def backward(self, dout: torch.Tensor):
+    def backward(self, dout: torch.Tensor, state: torch.Tensor | None = None):
+        """(dq, dk, dv) of the forward whose state is given (default: the last forward())."""
         m = self.model
+        state = self.saved if state is None else state
+        if state is None:
+            raise RuntimeError("backward called before forward")
         dout = dout.to(torch.bfloat16).contiguous()
         dq, dk, dv = self._empty(m.heads, dout), self._empty(m.kv_heads, dout), self._empty(m.kv_heads, dout)
-        _lib.call("a2d_bwd", self._ctx, dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
-                  torch.cuda.current_stream().cuda_stream)
+        _lib.call("a2d_bwd", self._ctx, state.data_ptr(), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                  dv.data_ptr(), torch.cuda.current_stream().cuda_stream)
         return dq, dk, dv
 
+    def sync(self, timeout_s: float = 600.0) -> None:
+        """Wait for this rank's queued layer work, polling NCCL for asynchronous
+        errors; raises (and aborts the communicators) on an error or timeout."""
+        _lib.call("a2d_sync", self._ctx, torch.cuda.current_stream().cuda_stream, int(timeout_s * 1000))
+
+    def lse_of(self, state: torch.Tensor) -> torch.Tensor:
+        """The natural-log LSE [Hl][C] fp32 (HeadSharded) inside a saved state."""
+        m, par = self.model, self.par
+        C = m.seq_len // par.d_cp
+        Hl = m.heads // par.d_hp
+        up = lambda x: (x + 255) // 256 * 256  # noqa: E731
+        from .config import replicated_kv_heads
+        hkl = replicated_kv_heads(m.kv_heads, par.d_hp, m.heads) // par.d_hp
+        off = up(Hl * C * 128 * 2) + up(2 * hkl * C * 128 * 2) + up(Hl * C * 128 * 2)
+        return state[off:off + Hl * C * 4].view(torch.float32).view(Hl, C)
     def close(self) -> None:
         if self._ctx:
             _lib.call("a2d_ctx_destroy", self._ctx)

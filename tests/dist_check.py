@@ -31,6 +31,40 @@ def metrics(got, ref):
             float(np.abs(ref).max()))
 
 
+def sampled_check(a, op, rank, qt, kt, vt, dot, out, dq, dk, dv):
+    """Gather the SeqSharded outputs (and the HeadSharded LSE of the plain
+    path) to global natural order on the GPU; rank 0 checks sampled rows/keys
+    of the first and last KV-head groups against the f64 oracle."""
+    from oracle import sampled
+
+    world = dist.get_world_size()
+
+    def gather_dev(x):
+        parts = [torch.empty_like(x) for _ in range(world)]
+        dist.all_gather(parts, x.contiguous())
+        return unshard_global(parts, op)
+
+    O, DQ, DK, DV = (gather_dev(x) for x in (out, dq, dk, dv))
+    LSE = None
+    if op.saved is not None and not a.fused_qkv and not a.native:
+        lse = op.saved[3].contiguous()  # HeadSharded (Hl, C): heads hp*Hl.., positions of CP chunk cp
+        parts = [torch.empty_like(lse) for _ in range(world)]
+        dist.all_gather(parts, lse)
+        LSE = torch.empty((a.heads, a.seq), dtype=torch.float32, device=lse.device)
+        for r, part in enumerate(parts):
+            hp, cp = op.grid.coords_of(r)
+            idx = op.plans[cp].pos.long()
+            LSE[hp * op.Hl:(hp + 1) * op.Hl][:, idx] = part
+    res = {}
+    if rank == 0:
+        res = sampled.check(qt, kt, vt, dot, O, DQ, DK, DV, LSE, causal=bool(a.causal), n_rows=a.rows,
+                            n_keys=a.keys, seed=a.seed)
+        res["violations"] = sampled.passes(res)
+        res["config"] = vars(a)
+        res["head_groups"] = op.ng
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--d-hp", type=int, required=True)
@@ -50,6 +84,14 @@ def main():
     ap.add_argument("--native", action="store_true",
                     help="run the native C++ runtime (C ABI a2d_ctx_create/a2d_fwd/a2d_bwd) instead of dist.Attn2D, "
                          "and also compare it with dist.Attn2D")
+    ap.add_argument("--two-layers", action="store_true",
+                    help="with --native: two layers' forwards in flight before their backwards (caller-owned "
+                         "saved states, stateless context); the checked layer runs first, the other in between")
+    ap.add_argument("--sampled", action="store_true",
+                    help="full-size check on sampled rows/keys (oracle/sampled.py) instead of the dense oracle; "
+                         "inputs drawn on the GPU (torch Philox, seeded) so S >= 16K, H = 32 fit")
+    ap.add_argument("--rows", type=int, default=512)
+    ap.add_argument("--keys", type=int, default=256)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
@@ -61,7 +103,14 @@ def main():
     par = ParallelConfig(d_hp=a.d_hp, d_cp=a.d_cp, inner_ring=a.w, placement=Placement(a.placement))
     op = Attn2D(model, par, ClusterConfig(), causal=bool(a.causal))
 
-    if a.golden:
+    dev = torch.device("cuda", local)
+    if a.sampled:
+        gen = torch.Generator(device=dev).manual_seed(a.seed)
+        qt = torch.randn((a.heads, a.seq, a.dim), device=dev, generator=gen).to(torch.bfloat16)
+        kt = torch.randn((a.kv_heads, a.seq, a.dim), device=dev, generator=gen).to(torch.bfloat16)
+        vt = torch.randn((a.kv_heads, a.seq, a.dim), device=dev, generator=gen).to(torch.bfloat16)
+        dot = torch.randn((a.heads, a.seq, a.dim), device=dev, generator=gen).to(torch.bfloat16)
+    elif a.golden:
         g = np.load(a.golden)
         to = lambda b: (np.asarray(b, np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
         q, k, v = (to(g[n]) for n in "qkv")
@@ -69,9 +118,9 @@ def main():
     else:
         q, k, v = orc.philox_qkv(a.seed, a.heads, a.kv_heads, a.seq, a.dim)
         do = np.random.Generator(np.random.Philox(a.seed + 1)).standard_normal(q.shape)
-    dev = torch.device("cuda", local)
     T = lambda x: torch.from_numpy(np.asarray(x, np.float32)).to(dev).to(torch.bfloat16)  # noqa: E731
-    qt, kt, vt, dot = T(q), T(k), T(v), T(do)
+    if not a.sampled:
+        qt, kt, vt, dot = T(q), T(k), T(v), T(do)
     if a.fused_qkv:
         H, Hkv = a.heads, a.kv_heads
         qkv = torch.cat([shard_global(x, op).transpose(0, 1) for x in (qt, kt, vt)], dim=1).contiguous()
@@ -86,8 +135,17 @@ def main():
         from paper_2406_18485_b200.native import NativeAttn2D
         nat = NativeAttn2D(model, par, ClusterConfig(), causal=bool(a.causal))
         args = [shard_global(x, op) for x in (qt, kt, vt)]
-        out = nat.forward(*args)
-        dq, dk, dv = nat.backward(shard_global(dot, op))
+        if a.two_layers:
+            out, st_a = nat.forward_with_state(*args)
+            args_b = [x.flip(-1).contiguous() for x in args]  # another layer's inputs
+            _, st_b = nat.forward_with_state(*args_b)
+            nat.backward(shard_global(dot, op).flip(-1).contiguous(), st_b)
+            dq, dk, dv = nat.backward(shard_global(dot, op), st_a)
+            del st_b
+        else:
+            out = nat.forward(*args)
+            dq, dk, dv = nat.backward(shard_global(dot, op))
+        nat.sync(300.0)
         ref_out = op.forward(*args)
         ref_grads = op.backward(shard_global(dot, op))
         torch.cuda.synchronize()
@@ -103,6 +161,17 @@ def main():
         parts = [torch.empty_like(x) for _ in range(dist.get_world_size())]
         dist.all_gather(parts, x.contiguous())
         return unshard_global(parts, op).float().cpu().numpy()
+
+    if a.sampled:
+        res = sampled_check(a, op, rank, qt, kt, vt, dot, out, dq, dk, dv)
+        if rank == 0:
+            print(json.dumps(res))
+            if a.out:
+                with open(a.out, "w") as f:
+                    json.dump(res, f)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
 
     O, DQ, DK, DV = (gather_all(x) for x in (out, dq, dk, dv))
     res = {}

@@ -5,6 +5,7 @@ Numerics: bf16 kernels vs f64 reference, max-abs <= 2e-2*max(1,|ref|) and
 rel-L2 <= 1e-2; layout ops bit-exact."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -149,3 +150,24 @@ def test_kv_replicate_contiguous_copies():
         assert torch.equal(c[2 * h], c[2 * h + 1])
     with pytest.raises(ValueError):
         A.kv_replicate(kv, 8, 64, 32)
+
+
+def test_verify_cli_lattice_and_fault_injection():
+    """tests/verify_cli.py mirrors the reference's `attn2d verify` (cli.py:46-122):
+    the whole lattice passes (exit 0), --inject-fault is detected (exit 1),
+    a bad S / d_sp combination is a config error (exit 2)."""
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cli = [sys.executable, os.path.join(root, "tests", "verify_cli.py")]
+    r = subprocess.run(cli, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "OK: all" in r.stdout
+    n = sum(1 for line in r.stdout.splitlines() if "max|delta|" in line)
+    assert n > 500  # the reference's lattice size (test_acceptance.py:53-91)
+    r = subprocess.run(cli + ["--seq", "32", "--inject-fault"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 1 and "FAIL" in r.stdout
+    r = subprocess.run(cli + ["--seq", "36", "--dsp", "4"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2

@@ -32,6 +32,12 @@ CASES = [
     (4, 1, 1, "head_first", 8, 2, 1024, 128),  # GQA replication: H_kv=2 < d_hp=4
     (2, 2, 2, "head_first", 4, 1, 1024, 128),  # replication AND a ring: the fp32 dK/dV home hop
     (2, 2, 2, "context_first", 8, 8, 1024, 64),
+    # 8 GPUs (BASELINE configs 3-5 grids at parity sizes)
+    (4, 2, 2, "head_first", 8, 8, 2048, 128),
+    (4, 2, 1, "context_first", 8, 8, 2048, 128),
+    (2, 4, 2, "head_first", 8, 2, 2048, 128),
+    (1, 8, 4, "context_first", 4, 4, 2048, 128),
+    (8, 1, 1, "head_first", 8, 4, 1024, 128),  # replication: H_kv=4 < d_hp=8
 ]
 
 
@@ -175,6 +181,8 @@ NATIVE = [
     (1, 4, 2, "head_first", 4, 4, 2048),
     (4, 1, 1, "context_first", 8, 2, 1024),   # GQA replication (H_kv < d_hp)
     (2, 2, 2, "head_first", 4, 1, 1024),      # replication and a ring: fp32 home hop
+    (4, 2, 2, "head_first", 8, 8, 2048),      # 8 GPUs: config 3's grid
+    (2, 4, 2, "context_first", 8, 2, 2048),   # 8 GPUs: config 4's grid (GQA, w=2)
 ]
 
 
@@ -194,3 +202,22 @@ def test_native_runtime_matches_oracle_and_python(case, tmp_path):
         assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
             f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
     assert res["native_vs_python"] <= 1e-2, res["native_vs_python"]
+
+
+@pytest.mark.parametrize("case", [(1, 1, 1, "head_first", 4, 2, 1024), (2, 2, 2, "context_first", 8, 4, 2048)],
+                         ids=lambda c: "x".join(map(str, c[:3])) + f"-{c[3]}")
+def test_native_two_layers_in_flight(case, tmp_path):
+    """Stateless context ABI: layer A's forward, layer B's forward, B's backward,
+    then A's backward from A's caller-owned saved state — A still matches the
+    oracle (ref ring.py:82-119 is a pure function)."""
+    d_hp, d_cp, w, pl, H, Hkv, S = case
+    n = d_hp * d_cp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    res = _run(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
+                   "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", "128", "--native",
+                   "--two-layers"], tmp_path, env={"A2D_TRANSPORT": "nccl"}, timeout=180)
+    for name in ("O", "dQ", "dK", "dV"):
+        ma, rl, rng = res[name]
+        assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
+            f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"

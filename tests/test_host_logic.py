@@ -148,8 +148,9 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"{s} declared in include/attn2d_sm100.h but not exported"
     loaded = _lib.load()
-    assert loaded.a2d_abi_version() == 1
-    assert set(_lib.SIGNATURES) | {"a2d_last_error", "a2d_abi_version"} == set(syms)
+    assert loaded.a2d_abi_version() == 2
+    assert set(_lib.SIGNATURES) | {"a2d_last_error", "a2d_abi_version", "a2d_launch_count"} == set(syms)
+    assert _lib.launch_count() == 0  # nothing launched without a GPU
 
 
 def test_library_rejects_bad_shapes_without_gpu():
@@ -310,3 +311,66 @@ def test_bench_reference_arm_contract():
     cb = line["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
     assert line["config"]["workload"].startswith("2D-Attention fwd+bwd") and line["config"]["global_tokens"] == 4096
+
+
+# ------------------------------------------------------------------ data-parallel replicas
+def _replica_worker(rank, world, port, d_hp, d_cp, interleave, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_18485_b200.config import ClusterConfig, ParallelConfig, build_rank_grid
+    from paper_2406_18485_b200.dist import make_groups
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_rep = world // (d_hp * d_cp)
+        reps = [list(range(r, world, n_rep)) if interleave else list(range(r * d_hp * d_cp, (r + 1) * d_hp * d_cp))
+                for r in range(n_rep)]
+        # each replica group created by all ranks (torch's rule), in the same order
+        pgs = [dist.new_group(r) for r in reps]
+        mine = next(i for i, r in enumerate(reps) if rank in r)
+        grid = build_rank_grid(ParallelConfig(d_hp=d_hp, d_cp=d_cp, inner_ring=1), ClusterConfig())
+        hp_group, ring, g_ranks = make_groups(grid, pgs[mine])
+        out = {"rank": rank, "replica": reps[mine], "g": g_ranks}
+        if hp_group is not None:
+            out["hp"] = sorted(dist.get_process_group_ranks(hp_group))
+            t = torch.tensor([rank])
+            dist.all_reduce(t, group=hp_group)  # traffic stays inside this replica's HP group
+            out["hp_sum"] = int(t)
+        if ring[0] is not None:
+            out["ring"] = [sorted(dist.get_process_group_ranks(g)) for g in ring]
+            t = torch.tensor([rank])
+            dist.all_reduce(t, group=ring[1])
+            out["ring_sum"] = int(t)
+        q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d_hp,d_cp,interleave", [(1, 2, False), (2, 1, True), (1, 2, True)])
+def test_make_groups_for_data_parallel_replicas(d_hp, d_cp, interleave):
+    """Two data-parallel replicas (d_dp = 2): every rank creates the HP
+    and ring groups of both replicas in one global order, so the groups are
+    consistent (no cross-wired or hanging communicators) and stay inside the
+    replica."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2 * d_hp * d_cp
+    port = 29650 + 10 * d_hp + d_cp + (5 if interleave else 0)
+    ps = [ctx.Process(target=_replica_worker, args=(r, world, port, d_hp, d_cp, interleave, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    for r in res:
+        assert r["g"] == r["replica"]
+        if "hp" in r:
+            assert set(r["hp"]) <= set(r["replica"]) and len(r["hp"]) == d_hp
+            assert r["hp_sum"] == sum(r["hp"])
+        if "ring" in r:
+            assert all(set(g) <= set(r["replica"]) and len(g) == d_cp for g in r["ring"])
+            assert r["ring_sum"] == sum(r["ring"][1])

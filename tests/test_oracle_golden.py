@@ -122,3 +122,46 @@ def test_gpu_pipeline_fixture_matches_oracle():
     for hf, name in ((True, "head_first"), (False, "context_first")):
         out = orc.two_d_attention(q, k, v, 8, 8, 2, 2, 2, hf, True)
         assert np.max(np.abs(out.values - g[f"out_{name}"])) <= 1e-5
+
+
+def test_row_and_key_restricted_grads_match_reference_golden():
+    """attention_grads_rows / attention_key_grads (the sampled large-S checks)
+    reproduce the reference's own attention_backward output (golden 'big' case,
+    causal, S=64) on every row / key subset we slice."""
+    g = golden("backward_small.npz")
+    q, k, v, do = (g[f"big_{n}"] for n in ("q", "k", "v", "do"))
+    pos = np.arange(q.shape[1])
+    out, lse = orc.attention(q, k, v, pos, pos, True)
+    delta = (do * out).sum(-1)
+    rows = np.array([0, 1, 17, 31, 32, 63])
+    dq = orc.attention_grads_rows(q, k, v, do[:, rows], pos, pos, rows, True)
+    assert np.max(np.abs(dq - g["big_dq"][:, rows])) <= 1e-10
+    keys = np.array([0, 5, 31, 62, 63])
+    dk, dv = orc.attention_key_grads(q, k, v, do, pos, pos, keys, lse, delta, True)
+    assert np.max(np.abs(dk - g["big_dk"][:, keys])) <= 1e-10
+    assert np.max(np.abs(dv - g["big_dv"][:, keys])) <= 1e-10
+
+
+@pytest.mark.parametrize("hkv", [1, 2])
+def test_sampled_check_is_exact_on_oracle_outputs(hkv):
+    """oracle/sampled.check (blocked f64 row statistics + sampled rows/keys)
+    reports ~0 error when fed the dense oracle's own outputs, and its f64 row
+    statistics pin to the oracle's LSE / delta."""
+    torch = pytest.importorskip("torch")
+    from oracle import sampled
+    H, S, d = 4, 384, 32
+    q, k, v = orc.philox_qkv(5, H, hkv, S, d)
+    do = np.random.Generator(np.random.Philox(6)).standard_normal(q.shape)
+    pos = np.arange(S)
+    out, lse = orc.attention(q, k, v, pos, pos, True)
+    dq, dk, dv = orc.attention_grads(q, k, v, do, pos, pos, True)
+    T = torch.from_numpy
+    res = sampled.check(T(q), T(k), T(v), T(do), T(out), T(dq), T(dk), T(dv), T(lse), causal=True,
+                        n_rows=64, n_keys=48, seed=3)
+    assert sampled.passes(res, max_abs=1e-10, rel_l2=1e-12, pin=1e-10) == [], res
+    assert res["rows"] >= 64 and res["keys"] >= 48
+    # a wrong dK column is caught
+    dk_bad = dk.copy()
+    dk_bad[:, 0] += 0.5
+    res = sampled.check(T(q), T(k), T(v), T(do), dk=T(dk_bad), causal=True, n_rows=16, n_keys=16, seed=3)
+    assert res["dK"][0] >= 0.49

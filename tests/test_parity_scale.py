@@ -1,0 +1,118 @@
+"""Parity at the sizes the north star and the bench name.
+
+The dense oracle cannot run at S >= 32K (H*S^2 scores), so these cases check
+the GPU run at full size on sampled query rows (O, LSE, dQ: exact f64 oracle
+rows) and sampled key columns (dK, dV: f64 oracle columns given every row's
+f64 LSE / delta, themselves pinned to the oracle) — ``oracle/sampled.py``.
+Rows/keys cover both sequence ends, 64/128-tile boundaries and every 1/16
+stripe edge (zig-zag stripe boundaries for d_cp <= 8) plus random fill.
+
+Bar (north star, ABSOLUTE): max-abs <= 2e-2 and rel-L2 <= 1e-2 per tensor;
+the f64 row statistics must match the oracle to 1e-9. Each case prints its
+per-tensor [max_abs, rel_l2, max|ref|] so the logs carry the numbers.
+"""
+
+import json
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# d_hp, d_cp, w, placement, H, H_kv, S, d, extra env
+SCALE_CASES = [
+    # 1 GPU: BASELINE config 2 (S=32K), the bench shape (config 3's S=128K), GQA at 64K
+    (1, 1, 1, "head_first", 32, 32, 32768, 128, {}),
+    (1, 1, 1, "head_first", 32, 32, 131072, 128, {}),
+    (1, 1, 1, "head_first", 32, 8, 65536, 128, {}),
+    # 2 GPUs
+    (2, 1, 1, "head_first", 32, 32, 32768, 128, {}),
+    (1, 2, 2, "context_first", 32, 8, 32768, 128, {}),
+    # 4 GPUs, both transports
+    (2, 2, 2, "head_first", 32, 32, 65536, 128, {}),
+    (2, 2, 2, "head_first", 32, 32, 65536, 128, {"A2D_TRANSPORT": "nccl"}),
+    (2, 2, 1, "context_first", 32, 8, 32768, 128, {}),
+    (1, 4, 2, "head_first", 32, 32, 32768, 128, {}),
+    (4, 1, 1, "context_first", 32, 2, 16384, 128, {}),  # GQA replication: H_kv=2 < d_hp=4
+    # 8 GPUs: config 3 (4x2, both placements, w=1/2), config 4 (GQA 2x4 w=2),
+    # 1x8 w=4, and 8x1 with replication (H_kv=4 < d_hp=8)
+    (4, 2, 2, "head_first", 32, 32, 65536, 128, {}),
+    (4, 2, 1, "context_first", 32, 32, 65536, 128, {}),
+    (4, 2, 2, "context_first", 32, 32, 32768, 128, {"A2D_TRANSPORT": "nccl"}),
+    (2, 4, 2, "head_first", 32, 8, 65536, 128, {}),
+    (1, 8, 4, "context_first", 32, 32, 32768, 128, {}),
+    (8, 1, 1, "head_first", 32, 4, 16384, 128, {}),
+]
+
+
+def _ids(c):
+    tag = "-nccl" if c[8].get("A2D_TRANSPORT") == "nccl" else ""
+    return f"{c[0]}x{c[1]}w{c[2]}-{c[3]}-H{c[4]}-{c[5]}-S{c[6]}-d{c[7]}{tag}"
+
+
+def run_sampled(n, args, env, tmp_path, timeout=900, port=29541):
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "dist_check.py"),
+           *args, "--sampled", "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env={**os.environ, **env})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return json.loads(out.read_text())
+
+
+@pytest.mark.parametrize("case", SCALE_CASES, ids=_ids)
+def test_sampled_parity_at_scale(case, tmp_path):
+    d_hp, d_cp, w, pl, H, Hkv, S, d, env = case
+    n = d_hp * d_cp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    res = run_sampled(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
+                          "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", str(d)],
+                      env, tmp_path)
+    print(_ids(case), json.dumps({k: res[k] for k in ("O", "LSE", "dQ", "dK", "dV", "pin_lse", "pin_delta")
+                                  if k in res}))
+    assert "LSE" in res and res["rows"] >= 512 and res["keys"] >= 256
+    assert res["violations"] == [], res
+
+
+@pytest.mark.parametrize("d_cp,w", [(2, 2), (4, 2), (4, 4)])
+def test_zigzag_double_ring_fold_at_32k(d_cp, w):
+    """api.run_double_ring (the reference's per-CP-rank fold, ring.py:64-79) on
+    zig-zag chunks of an S=32K, H=8 problem: every CP rank's folded O and LSE on
+    sampled rows (stripe boundaries included) vs the f64 oracle over all keys."""
+    from oracle import attn2d_oracle as orc
+    from oracle import sampled
+    from paper_2406_18485_b200 import api
+    dev = torch.device("cuda:0")
+    H, S, d = 8, 32768, 128
+    g = torch.Generator(device=dev).manual_seed(11)
+    q, k, v = (torch.randn((H, S, d), device=dev, generator=g).to(torch.bfloat16) for _ in range(3))
+    perm, _ = orc.zigzag(S, d_cp)
+    C = S // d_cp
+    chunks = lambda x: [api.DenseTensor(x[:, torch.as_tensor(perm[j * C:(j + 1) * C], device=dev)].contiguous(),  # noqa: E731
+                                        perm[j * C:(j + 1) * C]) for j in range(d_cp)]
+    res = api.run_double_ring(chunks(q), chunks(k), chunks(v), api.build_ring_schedule(d_cp, w), causal=True)
+    O = torch.empty((H, S, d), dtype=torch.float32, device=dev)
+    LSE = torch.empty((H, S), dtype=torch.float32, device=dev)
+    for j, r in enumerate(res):
+        idx = torch.as_tensor(perm[j * C:(j + 1) * C], device=dev)
+        O[:, idx] = r.out
+        LSE[:, idx] = r.lse
+    torch.cuda.synchronize()
+    rows = sampled.sample_indices(S, 512, 5)
+    qn, kn, vn = (x[[0, H - 1]].double().cpu().numpy() for x in (q, k, v))
+    pos = np.arange(S)
+    ro, rl = orc.attention_rows(qn, kn, vn, pos, pos, rows, True)
+    for name, got, ref in (("O", O[[0, H - 1]][:, rows].double().cpu().numpy(), ro),
+                           ("LSE", LSE[[0, H - 1]][:, rows].double().cpu().numpy(), rl)):
+        dd = np.abs(got - ref)
+        ma, rel = float(dd.max()), float(np.linalg.norm(dd) / np.linalg.norm(ref))
+        print(f"d_cp={d_cp} w={w} {name}: max-abs {ma:.3e} rel-L2 {rel:.3e}")
+        assert ma <= 2e-2 and rel <= 1e-2, (name, ma, rel)
