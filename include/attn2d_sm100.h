@@ -72,11 +72,11 @@ int a2d_bwd_preprocess(const void* o, const void* dout, const float* lse, int32_
 /* One ring step backward: gradients of the block (query chunk, KV chunk)
  * given the FINAL lse/delta of the query rows. Replaces the per-block part
  * of ref attention_backward (oracle.py:127-152):
- *   dq_acc (fp32, TRANSPOSED [H][128][Tq_pad], Tq_pad = round_up(Tq, 64),
+ *   dq_acc (fp32, TRANSPOSED [H][D][Tq_pad], Tq_pad = round_up(Tq, 64),
  *          query contiguous) += (dS K / sqrt(d))^T     (L2-side reduce-add);
- *          a2d_dqt_to_bf16 turns it into dQ
+ *          a2d_dqt_to_bf16(_d) turns it into dQ
  *   dk, dv [H_kv][Tk][D] (fp32) (+)= partial (accumulate_kv selects +=)
- * D must be 128 (pad smaller head dims with zeros and pass the true scale). */
+ * D must be 64 or 128 (pad other head dims with zeros and pass the true scale). */
 int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* dout, const int32_t* q_pos,
                      const int32_t* k_pos, const int32_t* q_bounds64, const int32_t* k_bounds128, const float* lse2,
                      const float* delta, float* dq_acc, float* dk, float* dv, int32_t accumulate_kv, int32_t H,
@@ -109,6 +109,13 @@ int a2d_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t 
                   int64_t dst_st, int64_t dst_sh, int64_t row_bytes, const int32_t* smap, const int32_t* dmap,
                   void* stream);
 
+/* Data-loader token gather of ref shard_sequence / unshard (sharding.py:56-106)
+ * over all H heads: scatter = 0: dst[h][t] = src[h][idx[t]]; scatter = 1:
+ * dst[h][idx[t]] = src[h][t]; t < L, rows of row_bytes (multiple of 16),
+ * head strides S_src / S_dst rows. Bit-exact byte move. */
+int a2d_gather_tokens(const void* src, void* dst, const int32_t* idx, int64_t H, int64_t S_src, int64_t L,
+                      int64_t S_dst, int64_t row_bytes, int32_t scatter, void* stream);
+
 /* dst[h] = sum_r src[h*rep + r] over per_head fp32 values (gradient of kv_replicate). */
 int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream);
 
@@ -122,6 +129,9 @@ int a2d_permute_f32_to_bf16(const float* src, void* dst, int64_t A, int64_t B, i
  * bf16(src[h][d][a*L + l]) with L = T/A; A = 1 gives [H][T][128], A = d_hp
  * gives the gradient all-to-all's peer-major pack (sharding.py:155-169). */
 int a2d_dqt_to_bf16(const float* src, void* dst, int32_t H, int64_t T, int64_t T_pad, int32_t A, void* stream);
+/* Same for a head dim D in {64, 128}: src [H][D][T_pad], dst [a][h][l][D]. */
+int a2d_dqt_to_bf16_d(const float* src, void* dst, int32_t H, int64_t T, int64_t T_pad, int32_t A, int32_t D,
+                      void* stream);
 
 /* Elementwise helpers (n multiple of 4). */
 int a2d_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);

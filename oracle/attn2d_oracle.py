@@ -134,7 +134,7 @@ def attention_grads(q, k, v, d_out, q_pos, k_pos, causal=False):
     return dq, dk_r.reshape(fold).sum(axis=1), dv_r.reshape(fold).sum(axis=1)
 
 
-def attention_grads_rows(q, k, v, d_out_rows, q_pos, k_pos, rows, causal=False):
+def attention_grads_rows(q, k, v, d_out_rows, q_pos, k_pos, rows, causal=False, bf16_ops=False):
     """dQ restricted to query rows ``rows`` — ref ``attention_backward``
     (oracle.py:127-152) evaluated on those rows only. Exact: every quantity of a
     dQ row (P, dP = dO V^T, row = sum(dP*P) at oracle.py:145, dS, dS K) depends
@@ -149,10 +149,21 @@ def attention_grads_rows(q, k, v, d_out_rows, q_pos, k_pos, rows, causal=False):
     kk = np.repeat(k, g, axis=0)
     dp = np.matmul(do, np.repeat(v, g, axis=0).transpose(0, 2, 1))
     ds = p * (dp - (dp * p).sum(axis=-1, keepdims=True))
+    if bf16_ops:  # dS enters the dQ GEMM as bf16 in the kernel
+        ds = bf16_round(ds)
     return np.matmul(ds, kk) * scale
 
 
-def attention_key_grads(q, k, v, d_out, q_pos, k_pos, keys, lse, delta, causal=False):
+def bf16_round(x):
+    """Round to the nearest bf16 (ties to even), returned as f64: emulates the
+    bf16 operands an MMA-based kernel feeds its tensor cores."""
+    x32 = np.ascontiguousarray(np.asarray(x, np.float32))
+    b = x32.view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def attention_key_grads(q, k, v, d_out, q_pos, k_pos, keys, lse, delta, causal=False, bf16_ops=False):
     """(dK, dV) restricted to key columns ``keys`` — ref ``attention_backward``
     (oracle.py:127-152) on those columns. A key column needs every query row's
     softmax statistics: ``lse`` (H, Tq) natural log (= the oracle's LSE) and
@@ -174,6 +185,8 @@ def attention_key_grads(q, k, v, d_out, q_pos, k_pos, keys, lse, delta, causal=F
     p = np.where(np.isneginf(s) | ~live[..., None], 0.0, p)
     dp = np.matmul(do, np.repeat(v, g, axis=0).transpose(0, 2, 1))
     ds = p * (dp - np.asarray(delta, np.float64)[..., None])
+    if bf16_ops:  # the kernel's precision policy: P and dS enter the dV / dK GEMMs as bf16
+        p, ds = bf16_round(p), bf16_round(ds)
     dk_r = np.matmul(ds.transpose(0, 2, 1), q) * scale
     dv_r = np.matmul(p.transpose(0, 2, 1), do)
     fold = (n_kv, g) + dk_r.shape[1:]

@@ -28,10 +28,12 @@ SIGNATURES = {
     "a2d_permute_blocks": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp],
     "a2d_gather_blocks": [_vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp],
     "a2d_sum_replicas_f32": [_vp, _vp, _c_i64, _c_i32, _c_i64, _vp],
+    "a2d_gather_tokens": [_vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i32, _vp],
     "a2d_copy_rows": [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp],
     "a2d_f32_to_bf16": [_vp, _vp, _c_i64, _vp],
     "a2d_permute_f32_to_bf16": [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp],
     "a2d_dqt_to_bf16": [_vp, _vp, _c_i32, _c_i64, _c_i64, _c_i32, _vp],
+    "a2d_dqt_to_bf16_d": [_vp, _vp, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _vp],
     "a2d_add_f32": [_vp, _vp, _c_i64, _vp],
     "a2d_selftest_umma": [_vp, _vp, _vp, _vp, _vp, _vp],
     "a2d_nccl_unique_id": [_vp, _c_i64],
@@ -83,7 +85,7 @@ def launch_count() -> int:
 # kernels each entry point launches (for the bench's gpu_launches accounting)
 LAUNCHES = {"a2d_tile_bounds": 1, "a2d_fa_fwd_chunk": 1, "a2d_bwd_preprocess": 1, "a2d_fa_bwd_chunk": 1,
             "a2d_merge": 1, "a2d_permute_blocks": 1, "a2d_gather_blocks": 1, "a2d_sum_replicas_f32": 1,
-            "a2d_f32_to_bf16": 1, "a2d_permute_f32_to_bf16": 1, "a2d_dqt_to_bf16": 1, "a2d_add_f32": 1, "a2d_selftest_umma": 1, "a2d_copy_rows": 1}
+            "a2d_f32_to_bf16": 1, "a2d_permute_f32_to_bf16": 1, "a2d_dqt_to_bf16": 1, "a2d_dqt_to_bf16_d": 1, "a2d_add_f32": 1, "a2d_selftest_umma": 1, "a2d_copy_rows": 1, "a2d_gather_tokens": 1}
 
 
 class LaunchLog:

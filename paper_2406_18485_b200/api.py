@@ -194,19 +194,23 @@ def attention_backward(q: DenseTensor, k: DenseTensor, v: DenseTensor, d_out,
     K.fwd_chunk(qp.t, kp.t, vp.t, qp.plan, kp.plan, causal, scale, lse, None, out)
     do = K.pad_dim(_as_torch(d_out).to(dev), kd)
     lse2, delta = K.bwd_preprocess(out, do, lse)
-    pad = lambda t: K.pad_dim(t, K.BWD_DIM)  # noqa: E731
-    dq_acc = K.dq_acc_t(H, T, dev)
-    dk = torch.empty((k.heads, k.tokens, K.BWD_DIM), dtype=torch.float32, device=dev)
+    dq_acc = K.dq_acc_t(H, T, dev, kd)
+    dk = torch.empty((k.heads, k.tokens, kd), dtype=torch.float32, device=dev)
     dv = torch.empty_like(dk)
-    K.bwd_chunk(pad(qp.t), pad(kp.t), pad(vp.t), pad(do), qp.plan, kp.plan, lse2, delta, dq_acc, dk, dv,
-                False, causal, scale)
+    K.bwd_chunk(qp.t, kp.t, vp.t, do, qp.plan, kp.plan, lse2, delta, dq_acc, dk, dv, False, causal, scale)
     return K.dq_from_acc(dq_acc, T)[..., :d], dk[..., :d], dv[..., :d]
 
 
 # ---------------------------------------------------------------- layout
 
 def _take_tokens(values, idx: np.ndarray):
+    """values[:, idx] (fresh). Device tensors with 16-byte-multiple token rows go
+    through the 128-bit gather_tokens kernel (the data-loader shard of ref
+    shard_sequence, sharding.py:56-79); host arrays stay numpy index shuffles."""
     if isinstance(values, torch.Tensor):
+        if values.is_cuda and values.dim() >= 2 and values.shape[1] > 0 and \
+                (values[0, 0].numel() * values.element_size()) % 16 == 0:
+            return K.gather_tokens(values, idx)
         return values[:, torch.as_tensor(idx, device=values.device)].contiguous()
     return values[:, idx].copy()
 

@@ -60,8 +60,12 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """profile=True: a separate lib/libattn2d_sm100_prof.so with -DA2D_PROFILE
+    (per-role barrier wait counters in the backward, a2d_prof_read); never
+    loaded by default."""
+    lib_out = LIB.replace(".so", "_prof.so") if profile else LIB
+    if not profile and not force and not needs_build():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
@@ -70,15 +74,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     objs = []
     for src in SOURCES:
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(BUILD, src.replace(".cu", "_prof.o" if profile else ".o"))
         objs.append(obj)
-        cmd = [cc, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-c",
-               os.path.join(CSRC, src), "-o", obj]
+        cmd = [cc, *ARCH, *FLAGS, *(["-DA2D_PROFILE"] if profile else []), "-I", os.path.join(ROOT, "include"),
+               "-I", nccl_inc, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     failed = []
     for src, p in procs:
         out, _ = p.communicate()
-        log = os.path.join(BUILD, src + ".log")
+        log = os.path.join(BUILD, src + ("_prof" if profile else "") + ".log")
         with open(log, "w") as f:
             f.write(out)
         if verbose:
@@ -88,22 +92,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         msg = "\n".join(f"--- {s}\n{o[-6000:]}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB + ".tmp"
+    tmp = lib_out + ".tmp"
     cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC", "-L", nccl_lib, "-l:libnccl.so.2",
            "-Xlinker", f"-rpath={nccl_lib}"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="build the instrumented lib/libattn2d_sm100_prof.so")
     a = ap.parse_args(argv)
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, profile=a.profile))
     return 0
 
 

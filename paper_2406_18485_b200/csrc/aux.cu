@@ -244,19 +244,20 @@ cudaError_t launch_permute_f32_bf16(const float* src, __nv_bfloat16* dst, int64_
 // dQ out of the backward's transposed accumulator: dst[a][h][l][d] =
 // bf16(src[h][d][a*L + l]), L = T/A (A = d_hp: the gradient all-to-all's pack;
 // A = 1: plain [h][t][d]). No shared memory: a block owns 128 tokens x all
-// 128 features of one head; warp w reads features 8w..8w+7 as float4 runs
+// D features of one head; warp w reads features 8w..8w+7 as float4 runs
 // along the tokens (each warp load = 512 contiguous bytes), transposes the
 // 8x4 register block and writes four 16-byte rows of 8 bf16 features. The 16
 // warps of a block together write every 256-byte token row, so the partial
 // lines merge in L2 before they reach DRAM.
-__global__ void __launch_bounds__(512) dqt_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
-                                                          int H, int64_t T, int64_t T_pad, int64_t L) {
+template <int D>
+__global__ void __launch_bounds__(D * 4) dqt_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                            int H, int64_t T, int64_t T_pad, int64_t L) {
   const int h = blockIdx.y;
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t t = (int64_t)blockIdx.x * 128 + 4 * lane;
   if (t >= T) return;
   const int f0 = 8 * w;
-  const float* s = src + ((size_t)h * 128 + f0) * T_pad + t;
+  const float* s = src + ((size_t)h * D + f0) * T_pad + t;
   float4 r[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) r[i] = __ldcs(reinterpret_cast<const float4*>(s + (size_t)i * T_pad));
@@ -270,19 +271,24 @@ __global__ void __launch_bounds__(512) dqt_to_bf16_kernel(const float* __restric
     __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
     __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]), p3 = __floats2bfloat162_rn(v[6], v[7]);
     const int64_t a = tok / L, l = tok % L;
-    *reinterpret_cast<uint4*>(dst + (((size_t)a * H + h) * L + l) * 128 + f0) =
+    *reinterpret_cast<uint4*>(dst + (((size_t)a * H + h) * L + l) * D + f0) =
         make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
                    *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
   }
 }
 
-cudaError_t launch_dqt_to_bf16(const float* src, __nv_bfloat16* dst, int H, int64_t T, int64_t T_pad, int A,
+cudaError_t launch_dqt_to_bf16(const float* src, __nv_bfloat16* dst, int H, int64_t T, int64_t T_pad, int A, int D,
                                cudaStream_t s) {
   if (H == 0 || T == 0) return cudaSuccess;
   if (T_pad % 4 || ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15))
     return cudaErrorInvalidValue;
   dim3 grid((unsigned)((T + 127) / 128), H);
-  dqt_to_bf16_kernel<<<grid, 512, 0, s>>>(src, dst, H, T, T_pad, T / A);
+  if (D == 128)
+    dqt_to_bf16_kernel<128><<<grid, 512, 0, s>>>(src, dst, H, T, T_pad, T / A);
+  else if (D == 64)
+    dqt_to_bf16_kernel<64><<<grid, 256, 0, s>>>(src, dst, H, T, T_pad, T / A);
+  else
+    return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
@@ -405,6 +411,36 @@ cudaError_t launch_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_
   if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
   copy_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n_t,
                                                     n_h, s_st, s_sh, d_st, d_sh, row_bytes / 16, smap, dmap);
+  return cudaGetLastError();
+}
+
+// Data-loader side of ref shard_sequence / unshard (sharding.py:56-106):
+// gather (dst[h][t] = src[h][idx[t]]) or scatter (dst[h][idx[t]] = src[h][t])
+// of whole token rows, row_vec x 16 bytes, 128-bit accesses, for every head.
+__global__ void gather_tokens_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, const int* __restrict__ idx,
+                                     int64_t H, int64_t S_src, int64_t L, int64_t S_dst, int64_t row_vec, int scatter) {
+  const int64_t total = H * L * row_vec;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i % row_vec;
+    const int64_t r = i / row_vec;
+    const int64_t t = r % L, h = r / L;
+    const int64_t j = __ldg(idx + t);
+    if (scatter)
+      dst[(h * S_dst + j) * row_vec + e] = __ldg(src + (h * S_src + t) * row_vec + e);
+    else
+      dst[(h * S_dst + t) * row_vec + e] = __ldg(src + (h * S_src + j) * row_vec + e);
+  }
+}
+
+cudaError_t launch_gather_tokens(const void* src, void* dst, const int* idx, int64_t H, int64_t S_src, int64_t L,
+                                 int64_t S_dst, int64_t row_bytes, int scatter, int n_sm, cudaStream_t s) {
+  if (row_bytes % 16 != 0) return cudaErrorInvalidValue;
+  const int64_t total = H * L * (row_bytes / 16);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  gather_tokens_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), idx, H,
+                                                        S_src, L, S_dst, row_bytes / 16, scatter);
   return cudaGetLastError();
 }
 

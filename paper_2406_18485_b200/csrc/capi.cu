@@ -28,7 +28,7 @@ cudaError_t launch_gather_blocks(const void* src, void* dst, const int* map, con
 cudaError_t launch_sum_replicas(const float* src, float* dst, int64_t heads, int rep, int64_t per_head, int n_sm,
                                 cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, int n_sm, cudaStream_t s);
-cudaError_t launch_dqt_to_bf16(const float* src, __nv_bfloat16* dst, int H, int64_t T, int64_t T_pad, int A,
+cudaError_t launch_dqt_to_bf16(const float* src, __nv_bfloat16* dst, int H, int64_t T, int64_t T_pad, int A, int D,
                                cudaStream_t s);
 cudaError_t launch_permute_f32_bf16(const float* src, __nv_bfloat16* dst, int64_t A, int64_t B, int64_t blk_elems,
                                     int n_sm, cudaStream_t s);
@@ -36,7 +36,8 @@ cudaError_t launch_add_f32(float* dst, const float* src, int64_t n, int n_sm, cu
 cudaError_t launch_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t s_st, int64_t s_sh,
                              int64_t d_st, int64_t d_sh, int64_t row_bytes, const int* smap, const int* dmap,
                              int n_sm, cudaStream_t s);
-
+cudaError_t launch_gather_tokens(const void* src, void* dst, const int* idx, int64_t H, int64_t S_src, int64_t L,
+                                 int64_t S_dst, int64_t row_bytes, int scatter, int n_sm, cudaStream_t s);
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};  // kernels launched through this library (a2d_launch_count)
@@ -189,7 +190,7 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
                      const int32_t* k_pos, const int32_t* q_bounds64, const int32_t* k_bounds128, const float* lse2,
                      const float* delta, float* dq_acc, float* dk, float* dv, int32_t accumulate_kv, int32_t H,
                      int32_t H_kv, int64_t Tq, int64_t Tk, int32_t D, int32_t causal, float scale, void* stream) {
-  if (D != 128) return fail(A2D_EINVAL, "a2d_fa_bwd_chunk: head dim must be 128 (zero-pad smaller dims)");
+  if (D != 128 && D != 64) return fail(A2D_EINVAL, "a2d_fa_bwd_chunk: head dim must be 64 or 128 (zero-pad others)");
   if (H <= 0 || H_kv <= 0 || H % H_kv != 0)
     return fail(A2D_EINVAL, std::to_string(H) + " query heads not divisible by " + std::to_string(H_kv) + " kv heads");
   if (Tq < 0 || Tk < 0 || Tq > INT32_MAX / 2 || Tk > INT32_MAX / 2) return fail(A2D_EINVAL, "a2d_fa_bwd_chunk: bad T");
@@ -210,8 +211,8 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
       const __nv_bfloat16* db = static_cast<const __nv_bfloat16*>(dout) + off * D;
       if ((rc = make_tmap_bf16_3d(&p.tm_q, qb, D, len, H, D, Tq * D, 64))) return rc;
       if ((rc = make_tmap_bf16_3d(&p.tm_do, db, D, len, H, D, Tq * D, 64))) return rc;
-      // dq_acc^T [H][128][tq_pad]: this slice starts at query `off`
-      if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc + off, len, D, H, tq_pad, (uint64_t)D * tq_pad, 32, 128)))
+      // dq_acc^T [H][D][tq_pad]: this slice starts at query `off`
+      if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc + off, len, D, H, tq_pad, (uint64_t)D * tq_pad, 32, D)))
         return rc;
     } else {
       p.tm_q = p.tm_k;
@@ -275,6 +276,18 @@ int a2d_copy_rows(const void* src, void* dst, int64_t n_t, int64_t n_h, int64_t 
                      "a2d_copy_rows");
 }
 
+int a2d_gather_tokens(const void* src, void* dst, const int32_t* idx, int64_t H, int64_t S_src, int64_t L,
+                      int64_t S_dst, int64_t row_bytes, int32_t scatter, void* stream) {
+  if (H < 0 || L < 0 || S_src < 0 || S_dst < 0 || row_bytes <= 0 || row_bytes % 16)
+    return fail(A2D_EINVAL, "a2d_gather_tokens: row_bytes must be a positive multiple of 16");
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(A2D_EINVAL, "a2d_gather_tokens: pointers must be 16-byte aligned");
+  if (L > 0 && !idx) return fail(A2D_EINVAL, "a2d_gather_tokens: idx is required");
+  return cuda_status(launch_gather_tokens(src, dst, idx, H, S_src, L, S_dst, row_bytes, scatter ? 1 : 0, sm_count(),
+                                          S(stream)),
+                     "a2d_gather_tokens");
+}
+
 int a2d_sum_replicas_f32(const float* src, float* dst, int64_t heads, int32_t rep, int64_t per_head, void* stream) {
   if (heads < 0 || rep <= 0 || per_head < 0) return fail(A2D_EINVAL, "a2d_sum_replicas_f32: bad shape");
   return cuda_status(launch_sum_replicas(src, dst, heads, rep, per_head, sm_count(), S(stream)),
@@ -298,9 +311,17 @@ int a2d_permute_f32_to_bf16(const float* src, void* dst, int64_t A, int64_t B, i
 }
 
 int a2d_dqt_to_bf16(const float* src, void* dst, int32_t H, int64_t T, int64_t T_pad, int32_t A, void* stream) {
-  if (H < 0 || T < 0 || T_pad < T || A <= 0 || T % A)
-    return fail(A2D_EINVAL, "a2d_dqt_to_bf16: need T_pad >= T and T divisible by A");
-  return cuda_status(launch_dqt_to_bf16(src, static_cast<__nv_bfloat16*>(dst), H, T, T_pad, A, S(stream)),
+  return a2d_dqt_to_bf16_d(src, dst, H, T, T_pad, A, 128, stream);
+}
+
+int a2d_dqt_to_bf16_d(const float* src, void* dst, int32_t H, int64_t T, int64_t T_pad, int32_t A, int32_t D,
+                      void* stream) {
+  if (H < 0 || T < 0 || T_pad < T || A <= 0 || T % A || T_pad % 4)
+    return fail(A2D_EINVAL, "a2d_dqt_to_bf16: need T_pad >= T, T_pad % 4 == 0 and T divisible by A");
+  if (D != 64 && D != 128) return fail(A2D_EINVAL, "a2d_dqt_to_bf16: head dim must be 64 or 128");
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(A2D_EINVAL, "a2d_dqt_to_bf16: pointers must be 16-byte aligned");
+  return cuda_status(launch_dqt_to_bf16(src, static_cast<__nv_bfloat16*>(dst), H, T, T_pad, A, D, S(stream)),
                      "a2d_dqt_to_bf16");
 }
 

@@ -35,25 +35,54 @@
 
 namespace a2d {
 
+// Optional wait-time instrumentation (build with -DA2D_PROFILE, see
+// build.py --profile): cycles each role spends blocked on each barrier,
+// summed over CTAs into g_bwd_prof[role*8 + slot] (role 0 MMA warp, 1 P/dS
+// warpgroup 0 (warp 4 lane 0), 2 dQ drain (warp 12 lane 0), 3 TMA producer).
+#ifdef A2D_PROFILE
+__device__ unsigned long long g_bwd_prof[32];
+#define PWAIT(bar, ph, slot)             \
+  do {                                   \
+    const long long t0_ = clock64();     \
+    mbar_wait(bar, ph);                  \
+    prof[slot] += clock64() - t0_;       \
+  } while (0)
+#define PSTART() const long long pt0_ = clock64()
+#define PFLUSH(role)                                                                            \
+  do {                                                                                          \
+    prof[7] = clock64() - pt0_;                                                                 \
+    if (lane == 0)                                                                              \
+      for (int s_ = 0; s_ < 8; ++s_) atomicAdd(&g_bwd_prof[(role) * 8 + s_], (unsigned long long)prof[s_]); \
+  } while (0)
+#else
+#define PWAIT(bar, ph, slot) mbar_wait(bar, ph)
+#define PSTART()
+#define PFLUSH(role)
+#endif
+
 namespace bwd {
 constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 64;   // queries per iteration
-constexpr int D = 128;
 constexpr int QST = 3;   // Q/dO stages (TMA latency off the critical path)
 constexpr int kThreads = 512;
 constexpr int kMaxQTiles = 4096;                 // live-list capacity per launch (the C ABI slices longer query chunks)
 constexpr uint16_t kFullBit = 0x8000;
-// smem layout (bytes, from 1 KB aligned base)
-constexpr int kK = 0;
-constexpr int kV = kK + BK * D * 2;              // 32 KB each
-constexpr int kQ = kV + BK * D * 2;              // QST x 16 KB
-constexpr int kDO = kQ + QST * BQ * D * 2;       // QST x 16 KB
-constexpr int kDS = kDO + QST * BQ * D * 2;      // 16 KB  (dS^T, [key][q] SW128)
-constexpr int kDQ = kDS + BK * BQ * 2;           // 32 KB fp32 dQ staging: 2 SW128 boxes [128 d][32 q]
-constexpr int kStats = kDQ + BQ * D * 4;         // QST x (lse2[64], delta[64])
-constexpr int kList = kStats + QST * 2 * BQ * 4; // live query tiles (int)
-constexpr int kEnd = kList + kMaxQTiles * 2;
-constexpr int kBytes = kEnd + 1024;
+// smem layout (bytes, from 1 KB aligned base) for head dim D (64 or 128)
+template <int D>
+struct Cfg {
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + BK * D * 2;              // 32 KB each at D = 128
+  static constexpr int kQ = kV + BK * D * 2;              // QST x 16 KB
+  static constexpr int kDO = kQ + QST * BQ * D * 2;       // QST x 16 KB
+  static constexpr int kDS = kDO + QST * BQ * D * 2;      // 16 KB  (dS^T, [key][q] SW128)
+  static constexpr int kDQ = kDS + BK * BQ * 2;           // fp32 dQ staging: 2 SW128 boxes [D][32 q]
+  static constexpr int kStats = kDQ + BQ * D * 4;         // QST x (lse2[64], delta[64])
+  static constexpr int kList = kStats + QST * 2 * BQ * 4; // live query tiles (uint16)
+  static constexpr int kEnd = kList + kMaxQTiles * 2;
+  static constexpr int kBytes = kEnd + 1024;
+  static constexpr int kPanels = D / 64;                  // 64-wide SW128 panels per row
+  static constexpr uint32_t kTdK = 256 + D;               // TMEM column of the dK accumulator (dV at 256)
+};
 }  // namespace bwd
 
 struct BwdBars {
@@ -74,8 +103,12 @@ A2D_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
       : "memory");
 }
 
+template <int D>
 __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_constant__ BwdParams p) {
   using namespace bwd;
+  using C = Cfg<D>;
+  constexpr int kK = C::kK, kV = C::kV, kQ = C::kQ, kDO = C::kDO, kDS = C::kDS, kDQ = C::kDQ;
+  constexpr int kStats = C::kStats, kList = C::kList;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   __shared__ BwdBars bars;
@@ -158,11 +191,14 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     regs_inc<152>();
   }
 
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  (void)prof;
   if (warp == 0) {
     // -------------------------------------------------------------- producer
+    PSTART();
     if (lane == 0 && n > 0) {
       mbar_expect_tx(&bars.kv_full, 2 * BK * D * 2);
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < C::kPanels; ++c) {
         tma_load_3d(smem + kK + c * 16384, &p.tm_k, &bars.kv_full, c * 64, key0, hk);
         tma_load_3d(smem + kV + c * 16384, &p.tm_v, &bars.kv_full, c * 64, key0, hk);
       }
@@ -172,9 +208,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         for (int li = 0; li < n_live; ++li, ++it) {
           const int qt = live_list[n_live - 1 - li] & (kFullBit - 1);
           const int qs = it % QST;
-          mbar_wait(&bars.qdo_empty[qs], ((it / QST) & 1) ^ 1);
+          PWAIT(&bars.qdo_empty[qs], ((it / QST) & 1) ^ 1, 0);
           mbar_expect_tx(&bars.qdo_full[qs], 2 * BQ * D * 2 + 2 * BQ * 4);
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < C::kPanels; ++c) {
             tma_load_3d(smem + kQ + qs * BQ * D * 2 + c * 8192, &p.tm_q, &bars.qdo_full[qs], c * 64, qt * BQ, h);
             tma_load_3d(smem + kDO + qs * BQ * D * 2 + c * 8192, &p.tm_do, &bars.qdo_full[qs], c * 64, qt * BQ,
                         h);
@@ -185,18 +221,23 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         }
       }
     }
+    PFLUSH(3);
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
     // The whole (converged) warp runs this loop so descriptors are computed in
     // uniform registers; an elected lane issues each group of tcgen05 ops.
+    PSTART();
     if (n > 0) {
       constexpr uint32_t id_s = idesc_bf16(BK, BQ, false, false);   // S^T, dP^T
       constexpr uint32_t id_kv = idesc_bf16(BK, D, false, true);    // dV, dK
-      constexpr uint32_t id_dq = idesc_bf16(D, BQ, true, true);     // dQ^T
+      // dQ^T: M = 128 feature rows always (rows >= D read the next smem panel
+      // and land in TMEM lanes the drain never reads: M = 64 would cost the
+      // same tensor time, max(M,128)*N/256 clocks per K16 step)
+      constexpr uint32_t id_dq = idesc_bf16(128, BQ, true, true);
       const uint32_t sK = smem_u32(smem + kK), sV = smem_u32(smem + kV);
       const uint32_t sQ = smem_u32(smem + kQ), sDO = smem_u32(smem + kDO);
       const uint32_t sDS = smem_u32(smem + kDS);
-      const uint32_t tDV = tmem + 256, tDK = tmem + 384;
+      const uint32_t tDV = tmem + 256, tDK = tmem + C::kTdK;
       // loop-invariant descriptor bases (the start-address field advances by bytes>>4)
       const uint64_t dK0 = sdesc_sw128(sK, 16, 1024), dV0 = sdesc_sw128(sV, 16, 1024);
       const uint64_t dQ0 = sdesc_sw128(sQ, 16, 1024), dDO0 = sdesc_sw128(sDO, 16, 1024);
@@ -220,16 +261,16 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         }
         __syncwarp();
       };
-      mbar_wait(&bars.kv_full, 0);
+      PWAIT(&bars.kv_full, 0, 0);
       for (int i = 0; i < 2 && i < n; ++i) {
-        mbar_wait(&bars.qdo_full[i % QST], (i / QST) & 1);
+        PWAIT(&bars.qdo_full[i % QST], (i / QST) & 1, 1);
         tc_fence_after();
         issue_s(i);
       }
       for (int i = 0; i < n; ++i) {
         const int b = i & 1, qs = i % QST;
         const uint64_t qoff = (uint64_t)((qs * BQ * D * 2) >> 4);
-        mbar_wait(&bars.ds_full[b], (i >> 1) & 1);
+        PWAIT(&bars.ds_full[b], (i >> 1) & 1, 2);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
@@ -253,8 +294,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         }
         __syncwarp();
         if (i + 2 < n) {
-          mbar_wait(&bars.dq_empty[b], (i >> 1) & 1);
-          mbar_wait(&bars.qdo_full[(i + 2) % QST], ((i + 2) / QST) & 1);
+          PWAIT(&bars.dq_empty[b], (i >> 1) & 1, 3);
+          PWAIT(&bars.qdo_full[(i + 2) % QST], ((i + 2) / QST) & 1, 1);
           tc_fence_after();
           issue_s(i + 2);
         }
@@ -263,6 +304,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       if (elect_one()) umma_commit(&bars.dkv_full);
       __syncwarp();
     }
+    PFLUSH(0);
   } else if (warp >= 12) {
     // ------------------------------------------------ dQ^T drain warpgroup
     // TMEM lane = feature d; 64 query columns -> two SW128 smem boxes -> TMA
@@ -270,8 +312,10 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     // P/dS warpgroups, off their critical path.
     const int wq = warp % 4;
     const int d = wq * 32 + lane;
+    const bool d_ok = d < D;  // D = 64: warps 14-15 only keep the barriers
+    PSTART();
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    float* dq_stage = reinterpret_cast<float*>(smem + kDQ);  // 2 boxes [128 d][32 q], SW128
+    float* dq_stage = reinterpret_cast<float*>(smem + kDQ);  // 2 boxes [D][32 q], SW128
     const bool leader = warp == 12 && lane == 0;
     const float scale = p.scale;
     int it = 0;
@@ -280,7 +324,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       for (int li = 0; li < n_live; ++li, ++it) {
         const int qt = live_list[n_live - 1 - li] & (kFullBit - 1);
         const int b = it & 1;
-        mbar_wait(&bars.dq_full[b], (it >> 1) & 1);
+        PWAIT(&bars.dq_full[b], (it >> 1) & 1, 0);
         tc_fence_after();
         uint32_t v0[32], v1[32];
         tmem_ld32(tmem + lane_base + b * 128 + 64, v0);
@@ -288,31 +332,40 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars.dq_empty[b]);
+#ifdef A2D_PROFILE
+        const long long tr0 = clock64();
+#endif
         if (leader) bulk_wait_read0();  // previous reduce finished reading the stage
+#ifdef A2D_PROFILE
+        prof[1] += clock64() - tr0;
+#endif
         named_bar_sync(1, 128);
         // box b = queries [32b, 32b+32) x all 128 features, SW128: row d, 16-byte
         // chunk j (queries 4j..4j+3) at position j ^ (d & 7)
-        uint8_t* st = reinterpret_cast<uint8_t*>(dq_stage) + d * 128;
+        if (d_ok) {
+          uint8_t* st = reinterpret_cast<uint8_t*>(dq_stage) + d * 128;
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<float4*>(st + ((c ^ (d & 7)) << 4)) =
-              make_float4(__uint_as_float(v0[4 * c]) * scale, __uint_as_float(v0[4 * c + 1]) * scale,
-                          __uint_as_float(v0[4 * c + 2]) * scale, __uint_as_float(v0[4 * c + 3]) * scale);
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(st + ((c ^ (d & 7)) << 4)) =
+                make_float4(__uint_as_float(v0[4 * c]) * scale, __uint_as_float(v0[4 * c + 1]) * scale,
+                            __uint_as_float(v0[4 * c + 2]) * scale, __uint_as_float(v0[4 * c + 3]) * scale);
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<float4*>(st + 16384 + ((c ^ (d & 7)) << 4)) =
-              make_float4(__uint_as_float(v1[4 * c]) * scale, __uint_as_float(v1[4 * c + 1]) * scale,
-                          __uint_as_float(v1[4 * c + 2]) * scale, __uint_as_float(v1[4 * c + 3]) * scale);
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(st + D * 128 + ((c ^ (d & 7)) << 4)) =
+                make_float4(__uint_as_float(v1[4 * c]) * scale, __uint_as_float(v1[4 * c + 1]) * scale,
+                            __uint_as_float(v1[4 * c + 2]) * scale, __uint_as_float(v1[4 * c + 3]) * scale);
+        }
         fence_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
           tma_reduce_add_3d(&p.tm_dq, dq_stage, qt * BQ, 0, h);
-          tma_reduce_add_3d(&p.tm_dq, dq_stage + 4096, qt * BQ + 32, 0, h);
+          tma_reduce_add_3d(&p.tm_dq, dq_stage + D * 32, qt * BQ + 32, 0, h);
           bulk_commit();
         }
       }
     }
     if (leader) bulk_wait0();
+    if (warp == 12) PFLUSH(2);
   } else if (warp >= 4) {
     // ------------------------------------------------ P/dS warpgroups
     // Both warpgroups cover all 128 key rows (TMEM lanes); warpgroup hq owns
@@ -328,6 +381,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     const int c0 = hq * 32;
     const int* qpos_base = p.q_pos;
     const int Tq = p.Tq;
+    PSTART();
     int it = 0;
     for (int g = 0; g < p.G; ++g) {
       for (int li = 0; li < n_live; ++li, ++it) {
@@ -335,9 +389,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         const int qt = ent & (kFullBit - 1);
         const bool full = (ent & kFullBit) != 0;
         const int b = it & 1, qs = it % QST;
-        mbar_wait(&bars.qdo_full[qs], (it / QST) & 1);  // stats landed with the TMA stage
+        PWAIT(&bars.qdo_full[qs], (it / QST) & 1, 0);  // stats landed with the TMA stage
         const float4* st4 = reinterpret_cast<const float4*>(smem + kStats + qs * 2 * BQ * 4);
-        mbar_wait(&bars.s_full[b], (it >> 1) & 1);
+        PWAIT(&bars.s_full[b], (it >> 1) & 1, 1);
         tc_fence_after();
         uint32_t sr[32], dr[32];
         tmem_ld32(tmem + lane_base + b * 128 + c0, sr);
@@ -392,7 +446,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         // [c0, c0+16) and [c0+16, c0+32) — the TMEM A operands of dV and dK
         tmem_st16(tmem + lane_base + b * 128 + c0, pw);
         tmem_st16(tmem + lane_base + b * 128 + c0 + 16, dw);
-        if (it >= 1) mbar_wait(&bars.ds_free, (it - 1) & 1);  // dQ^T of it-1 done reading dS
+        if (it >= 1) PWAIT(&bars.ds_free, (it - 1) & 1, 2);  // dQ^T of it-1 done reading dS
         uint8_t* dsrow = smem + kDS;
 #pragma unroll
         for (int c8 = 0; c8 < 4; ++c8)
@@ -404,6 +458,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         mbar_arrive(&bars.ds_full[b]);
       }
     }
+    if (warp == 4) PFLUSH(1);
     // ------------------------------------------------ dV (hq=0) / dK (hq=1) epilogue
     if (n > 0) {
       mbar_wait(&bars.dkv_full, 0);
@@ -415,7 +470,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     for (int c = 0; c < D / 32; ++c) {
       uint32_t rr[32];
       if (n > 0) {
-        tmem_ld32(tmem + lane_base + 256 + hq * 128 + c * 32, rr);
+        tmem_ld32(tmem + lane_base + 256 + hq * D + c * 32, rr);
         tmem_ld_wait();
       } else {
 #pragma unroll
@@ -442,15 +497,30 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
-  if (head_dim != 128) return cudaErrorInvalidValue;
-  if (p.Tk <= 0 || p.Hkv <= 0) return cudaSuccess;
-  if ((p.Tq + bwd::BQ - 1) / bwd::BQ > bwd::kMaxQTiles) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd::kBytes);
+template <int D>
+static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
+  constexpr int bytes = bwd::Cfg<D>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(fa_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   dim3 grid((p.Tk + bwd::BK - 1) / bwd::BK, p.Hkv);
-  fa_bwd_kernel<<<grid, bwd::kThreads, bwd::kBytes, s>>>(p);
+  fa_bwd_kernel<D><<<grid, bwd::kThreads, bytes, s>>>(p);
   return cudaGetLastError();
 }
 
+cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
+  if (head_dim != 128 && head_dim != 64) return cudaErrorInvalidValue;
+  if (p.Tk <= 0 || p.Hkv <= 0) return cudaSuccess;
+  if ((p.Tq + bwd::BQ - 1) / bwd::BQ > bwd::kMaxQTiles) return cudaErrorInvalidValue;
+  return head_dim == 128 ? launch_bwd_d<128>(p, s) : launch_bwd_d<64>(p, s);
+}
+
 }  // namespace a2d
+
+#ifdef A2D_PROFILE
+extern "C" int a2d_prof_read(unsigned long long* out, int n) {
+  if (n > 32) n = 32;
+  if (cudaMemcpyFromSymbol(out, a2d::g_bwd_prof, n * sizeof(unsigned long long)) != cudaSuccess) return 2;
+  unsigned long long z[32] = {0};
+  return cudaMemcpyToSymbol(a2d::g_bwd_prof, z, sizeof(z)) == cudaSuccess ? 0 : 2;
+}
+#endif

@@ -220,7 +220,6 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
   const int n = bars.n_live;
-
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0 && n > 0) {
@@ -388,31 +387,30 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       const float neg_m = m_used == -INFINITY ? 0.f : -m_used;
       const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
       float2 part[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      uint32_t pk[BN / 2];
+      // P in 32-column chunks, each stored to TMEM (16 bf16 pairs) as soon as
+      // it is packed: the packed P never has to be live all at once (no spills)
 #pragma unroll
-      for (int c = 0; c < BN; c += 2) {
-        const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl2x2, nm2);
-        float2 e;
-        if (((c / 2) & 3) == 3) {  // one pair in four on the FMA pipe (MUFU relief)
-          e = ex2_poly2(x);
-        } else {
-          e.x = ex2(x.x);
-          e.y = ex2(x.y);
+      for (int cc = 0; cc < BN; cc += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = cc; c < cc + 32; c += 2) {
+          const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl2x2, nm2);
+          float2 e;
+          if (((c / 2) & 3) == 3) {  // one pair in four on the FMA pipe (MUFU relief)
+            e = ex2_poly2(x);
+          } else {
+            e.x = ex2(x.x);
+            e.y = ex2(x.y);
+          }
+          part[(c / 2) & 3] = __fadd2_rn(part[(c / 2) & 3], e);
+          pk[(c - cc) / 2] = pack_bf16(e.x, e.y);
         }
-        part[(c / 2) & 3] = __fadd2_rn(part[(c / 2) & 3], e);
-        pk[c / 2] = pack_bf16(e.x, e.y);
+        tmem_st16(tS + cc / 2, pk);
       }
       {
         const float2 p01 = __fadd2_rn(part[0], part[1]), p23 = __fadd2_rn(part[2], part[3]);
         const float2 pt = __fadd2_rn(p01, p23);
         l_sum += pt.x + pt.y;
-      }
-#pragma unroll
-      for (int c = 0; c < BN / 64; ++c) {
-        uint32_t r[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = pk[c * 32 + i];
-        tmem_st32(tS + c * 32, r);
       }
       if (__any_sync(0xffffffffu, rescale)) {
         // O (this tile's previous PV) is complete: s_full's commit tracks it.

@@ -140,7 +140,7 @@ class Attn2D:
         S, H, Hkv = model.seq_len, model.heads, model.kv_heads
         self.d = model.head_dim
         self.kd = K.fwd_dim(self.d)
-        self.bd = K.BWD_DIM
+        self.bd = self.kd  # backward kernel head dim (64 or 128, zero-padded like the forward)
         self.scale = 1.0 / math.sqrt(self.d)
         self.H_rep = replicated_kv_heads(Hkv, d_hp, H)
         if self.H_rep % d_hp != 0:
@@ -830,20 +830,20 @@ class Attn2DFunction(torch.autograd.Function):
 
 
 def shard_global(x: torch.Tensor, op: Attn2D) -> torch.Tensor:
-    """This rank's SeqSharded chunk of a global (H, S, d) tensor (ref shard_sequence)."""
-    idx = torch.as_tensor(op.seq_pos, device=x.device)
-    return x[:, idx].contiguous()
+    """This rank's SeqSharded chunk of a global (H, S, d) tensor (ref shard_sequence,
+    sharding.py:56-79): the 128-bit gather_tokens kernel."""
+    return K.gather_tokens(x, op.seq_pos)
 
 
 def unshard_global(chunks: list[torch.Tensor], op: Attn2D) -> torch.Tensor:
-    """Reassemble global (H, S, d) from all ranks' SeqSharded chunks (ref unshard)."""
+    """Reassemble global (H, S, d) from all ranks' SeqSharded chunks (ref unshard,
+    sharding.py:91-106): one gather_tokens scatter per chunk."""
     S = op.model.seq_len
     out = torch.empty((chunks[0].shape[0], S) + tuple(chunks[0].shape[2:]), dtype=chunks[0].dtype,
                       device=chunks[0].device)
     for r, c in enumerate(chunks):
         hp, cp = op.grid.coords_of(r)
-        idx = torch.as_tensor(seq_positions(S, op.grid, hp, cp), device=c.device)
-        out[:, idx] = c
+        K.gather_tokens(c, seq_positions(S, op.grid, hp, cp), out=out, scatter=True)
     return out
 
 

@@ -15,7 +15,8 @@ from . import _lib
 
 BF16 = torch.bfloat16
 FWD_DIMS = (64, 128)
-BWD_DIM = 128
+BWD_DIMS = (64, 128)
+BWD_DIM = 128  # the native runtime's head dim
 BWD_QSLICE = 4096 * 64  # query rows per fa_bwd launch (capi.cu a2d_fa_bwd_chunk)
 
 
@@ -101,9 +102,9 @@ def bwd_preprocess(o: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor):
     return lse2, delta
 
 
-def dq_acc_t(H: int, T: int, device) -> torch.Tensor:
-    """Zeroed transposed dQ accumulator [H][128][round_up(T, 64)] fp32 (bwd_chunk's dq_acc)."""
-    return torch.zeros((H, BWD_DIM, (T + 63) // 64 * 64), dtype=torch.float32, device=device)
+def dq_acc_t(H: int, T: int, device, D: int = BWD_DIM) -> torch.Tensor:
+    """Zeroed transposed dQ accumulator [H][D][round_up(T, 64)] fp32 (bwd_chunk's dq_acc)."""
+    return torch.zeros((H, D, (T + 63) // 64 * 64), dtype=torch.float32, device=device)
 
 
 def dq_from_acc(acc: torch.Tensor, T: int) -> torch.Tensor:
@@ -113,25 +114,25 @@ def dq_from_acc(acc: torch.Tensor, T: int) -> torch.Tensor:
 
 def dqt_to_bf16(acc: torch.Tensor, T: int, A: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
     """bf16 dQ out of the transposed accumulator: out[a][h][l][:] = acc[h][:][a*L + l], L = T/A."""
-    H = acc.shape[0]
+    H, D = acc.shape[0], acc.shape[1]
     if out is None:
-        out = torch.empty((A, H, T // A, BWD_DIM), dtype=BF16, device=acc.device)
-    _lib.call("a2d_dqt_to_bf16", acc.data_ptr(), out.data_ptr(), H, T, acc.shape[2], A, _stream(),
-              nbytes=H * T * BWD_DIM * 6)
+        out = torch.empty((A, H, T // A, D), dtype=BF16, device=acc.device)
+    _lib.call("a2d_dqt_to_bf16_d", acc.data_ptr(), out.data_ptr(), H, T, acc.shape[2], A, D, _stream(),
+              nbytes=H * T * D * 6)
     return out
 
 
 def bwd_chunk(q, k, v, dout, qp: ChunkPlan, kp: ChunkPlan, lse2, delta, dq_acc, dk, dv,
               accumulate_kv: bool, causal: bool, scale: float) -> None:
-    """One ring step backward (K3). q/k/v/dout bf16 D=128; dk/dv fp32 [H_kv][Tk][128];
-    dq_acc fp32 TRANSPOSED [H][128][round_up(Tq, 64)] (see dq_acc_t / dqt_to_bf16)."""
+    """One ring step backward (K3). q/k/v/dout bf16 D in {64, 128}; dk/dv fp32 [H_kv][Tk][D];
+    dq_acc fp32 TRANSPOSED [H][D][round_up(Tq, 64)] (see dq_acc_t / dqt_to_bf16)."""
     H, Tq, D = q.shape
     Hkv, Tk, _ = k.shape
     n_launch = max(1, -(-Tq // BWD_QSLICE)) if Tk > 0 else 0  # the C ABI slices long query chunks
-    if D != BWD_DIM:
-        raise ValueError("backward kernel head dim must be 128")
-    if dq_acc.shape != (H, BWD_DIM, (Tq + 63) // 64 * 64) or dq_acc.dtype != torch.float32:
-        raise ValueError("dq_acc must be the transposed fp32 accumulator [H][128][round_up(Tq, 64)]")
+    if D not in BWD_DIMS:
+        raise ValueError("backward kernel head dim must be 64 or 128")
+    if dq_acc.shape != (H, D, (Tq + 63) // 64 * 64) or dq_acc.dtype != torch.float32:
+        raise ValueError("dq_acc must be the transposed fp32 accumulator [H][D][round_up(Tq, 64)]")
     _lib.call("a2d_fa_bwd_chunk", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
               qp.pos.data_ptr(), kp.pos.data_ptr(), qp.b64.data_ptr(), kp.b128.data_ptr(),
               lse2.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dk.data_ptr(), dv.data_ptr(),
@@ -190,6 +191,27 @@ def copy_rows(src: torch.Tensor, dst: torch.Tensor, src_map: torch.Tensor | None
               dst.stride(0) * es, dst.stride(1) * es, row, None if sm is None else sm.data_ptr(),
               None if dm is None else dm.data_ptr(), _stream(), nbytes=2 * n_t * n_h * row)
     return dst
+
+
+def gather_tokens(src: torch.Tensor, idx, out: torch.Tensor | None = None, scatter: bool = False,
+                  out_tokens: int | None = None) -> torch.Tensor:
+    """Token rows of every head (ref shard_sequence / unshard, sharding.py:56-106):
+    gather out[h][t] = src[h][idx[t]], or scatter out[h][idx[t]] = src[h][t].
+    src (H, S, ...) contiguous with 16-byte-multiple rows; any dtype (byte move)."""
+    _check_cuda(src)
+    src = src.contiguous()
+    idx = torch.as_tensor(idx, device=src.device).to(torch.int32).contiguous()
+    H, S = src.shape[0], src.shape[1]
+    row = src[0, 0].numel() * src.element_size() if S else 16
+    L = idx.numel()
+    if out is None:
+        n = (out_tokens if out_tokens is not None else S) if scatter else L
+        out = torch.empty((H, n) + tuple(src.shape[2:]), dtype=src.dtype, device=src.device)
+    if row % 16 or out.dtype != src.dtype or not out.is_contiguous():
+        raise ValueError("gather_tokens needs contiguous same-dtype tensors with 16-byte-multiple rows")
+    _lib.call("a2d_gather_tokens", src.data_ptr(), out.data_ptr(), idx.data_ptr(), H, S, L, out.shape[1], row,
+              int(scatter), _stream(), nbytes=2 * H * L * row)
+    return out
 
 
 def sum_replicas(src: torch.Tensor, rep: int) -> torch.Tensor:

@@ -166,7 +166,11 @@ def test_verify_cli_lattice_and_fault_injection():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "OK: all" in r.stdout
     n = sum(1 for line in r.stdout.splitlines() if "max|delta|" in line)
-    assert n > 500  # the reference's lattice size (test_acceptance.py:53-91)
+    assert n == 304  # the reference verify lattice (cli.py:58-91): 2 H_kv x 2 S x 2 causal x 38 grids
+    r = subprocess.run(cli + ["--acceptance"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    n = sum(1 for line in r.stdout.splitlines() if "max|delta|" in line)
+    assert n > 500  # acceptance criterion 1's lattice (test_acceptance.py:53-91)
     r = subprocess.run(cli + ["--seq", "32", "--inject-fault"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 1 and "FAIL" in r.stdout
     r = subprocess.run(cli + ["--seq", "36", "--dsp", "4"], capture_output=True, text=True, timeout=120)

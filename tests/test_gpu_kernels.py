@@ -130,10 +130,13 @@ def test_fwd_zigzag_steps_and_merge(d_cp):
         close(f"rank {j} LSE", lse.cpu().numpy(), rl[:, qpos])
 
 
-def _bwd(q, k, v, do, q_pos, k_pos, causal, device):
+def _bwd(q, k, v, do, q_pos, k_pos, causal, device, bd=None):
+    """Forward then backward chunk; the backward runs at head dim bd (default:
+    the forward's 64 / 128 kernel dim, i.e. the d=64 kernel for d <= 64)."""
     from paper_2406_18485_b200 import kernels as K
     D = q.shape[-1]
     fd = K.fwd_dim(D)
+    bd = bd or fd
     H, T = q.shape[0], q.shape[1]
     Hkv, Tk = k.shape[0], k.shape[1]
     t = lambda x, dd: K.pad_dim(torch.from_numpy(np.asarray(x, np.float32)).to(device), dd)  # noqa: E731
@@ -145,10 +148,10 @@ def _bwd(q, k, v, do, q_pos, k_pos, causal, device):
     K.fwd_chunk(t(q, fd), t(k, fd), t(v, fd), qp, kp, causal, scale, lse, None, out)
     dot = t(do, fd)
     lse2, delta = K.bwd_preprocess(out, dot, lse)
-    dq_acc = K.dq_acc_t(H, T, device)
-    dk = torch.empty((Hkv, Tk, 128), dtype=torch.float32, device=device)
-    dv = torch.empty((Hkv, Tk, 128), dtype=torch.float32, device=device)
-    K.bwd_chunk(t(q, 128), t(k, 128), t(v, 128), t(do, 128), qp, kp, lse2, delta, dq_acc, dk, dv, False,
+    dq_acc = K.dq_acc_t(H, T, device, bd)
+    dk = torch.empty((Hkv, Tk, bd), dtype=torch.float32, device=device)
+    dv = torch.empty((Hkv, Tk, bd), dtype=torch.float32, device=device)
+    K.bwd_chunk(t(q, bd), t(k, bd), t(v, bd), t(do, bd), qp, kp, lse2, delta, dq_acc, dk, dv, False,
                 causal, scale)
     torch.cuda.synchronize()
     dq = K.dq_from_acc(dq_acc, T)
@@ -168,7 +171,8 @@ def test_bwd_chunk_golden(name):
 
 
 @pytest.mark.parametrize("causal", [False, True])
-@pytest.mark.parametrize("shape", [(4, 2, 768, 128), (2, 2, 130, 128)])
+@pytest.mark.parametrize("shape", [(4, 2, 768, 128), (2, 2, 130, 128), (4, 2, 768, 64), (2, 1, 333, 64),
+                                   (2, 2, 200, 48)])
 def test_bwd_chunk_oracle(shape, causal):
     d = dev()
     H, Hkv, T, D = shape
@@ -180,6 +184,22 @@ def test_bwd_chunk_oracle(shape, causal):
     close("dQ", dq, rq)
     close("dK", dk, rk)
     close("dV", dv, rv)
+
+
+def test_bwd_d64_kernel_matches_padded_d128():
+    """The D=64 backward instantiation (BASELINE config 1's head dim) against
+    the same gradients from the zero-padded D=128 kernel and the oracle."""
+    d = dev()
+    H, Hkv, T, D = 4, 2, 640, 64
+    q, k, v = (bf16_round(x) for x in orc.philox_qkv(5, H, Hkv, T, D))
+    do = bf16_round(np.random.Generator(np.random.Philox(6)).standard_normal(q.shape))
+    pos = np.arange(T)
+    g64 = _bwd(q, k, v, do, pos, pos, True, d)
+    g128 = _bwd(q, k, v, do, pos, pos, True, d, bd=128)
+    ref = orc.attention_grads(q, k, v, do, pos, pos, True)
+    for name, a, b, r in zip(("dQ", "dK", "dV"), g64, g128, ref):
+        close(name + " d64", a, r)
+        assert np.max(np.abs(a - b)) <= 1e-3 * max(1.0, np.abs(r).max()), name
 
 
 def test_permute_and_gather_bit_exact():
@@ -238,3 +258,38 @@ def test_bwd_query_slicing_beyond_one_launch():
     close("dQ (sampled rows)", dq[:, rows], rq[:, rows])
     close("dK", dk, rk)
     close("dV", dv, rv)
+
+
+def test_gather_tokens_bit_exact_and_shard_roundtrip():
+    """a2d_gather_tokens (data-loader shard of ref shard_sequence / unshard,
+    sharding.py:56-106): gather and scatter are bit-exact byte moves, and the
+    global-view shard -> unshard through it is the identity for bf16 d=128."""
+    from paper_2406_18485_b200 import api
+    from paper_2406_18485_b200 import kernels as K
+    from paper_2406_18485_b200.config import ClusterConfig, ParallelConfig, Placement, build_rank_grid
+    d = dev()
+    x = torch.randint(-2**15, 2**15, (3, 96, 128), dtype=torch.int16, device=d).view(torch.bfloat16)
+    idx = torch.randperm(96, device=d)[:40]
+    got = K.gather_tokens(x, idx)
+    assert torch.equal(got.view(torch.int16), x.view(torch.int16)[:, idx.long()])
+    back = torch.zeros_like(x)
+    K.gather_tokens(got, idx, out=back, scatter=True)
+    ref = torch.zeros_like(x)
+    ref[:, idx.long()] = x[:, idx.long()]
+    assert torch.equal(back.view(torch.int16), ref.view(torch.int16))
+    S = 256
+    vals = torch.randn(4, S, 128, device=d).to(torch.bfloat16)
+    pos = np.arange(S)
+    for d_hp, d_cp in ((2, 2), (1, 4), (4, 1)):
+        for pl in Placement:
+            grid = build_rank_grid(ParallelConfig(d_hp=d_hp, d_cp=d_cp, placement=pl), ClusterConfig())
+            sh = api.shard_sequence(api.DenseTensor(vals, pos), grid)
+            perm, _ = orc.zigzag(S, d_cp)
+            for j in range(d_cp):
+                for i in range(d_hp):
+                    c = sh.chunk(i, j)
+                    L = S // (d_hp * d_cp)
+                    want = perm[j * (S // d_cp) + i * L: j * (S // d_cp) + (i + 1) * L]
+                    assert np.array_equal(c.positions, want)
+                    assert torch.equal(c.values, vals[:, torch.as_tensor(want, device=d)])
+            assert torch.equal(api.unshard(sh).values, vals)

@@ -165,3 +165,14 @@ def test_sampled_check_is_exact_on_oracle_outputs(hkv):
     dk_bad[:, 0] += 0.5
     res = sampled.check(T(q), T(k), T(v), T(do), dk=T(dk_bad), causal=True, n_rows=16, n_keys=16, seed=3)
     assert res["dK"][0] >= 0.49
+
+
+def test_bf16_round_matches_torch():
+    """bf16_round (the kernel precision-policy emulation used by the sampled
+    gradient checks) is torch's round-to-nearest-even bf16 conversion."""
+    torch = pytest.importorskip("torch")
+    x = np.random.Generator(np.random.Philox(9)).standard_normal(100000) * np.exp(
+        np.random.Generator(np.random.Philox(10)).uniform(-20, 20, 100000))
+    x = np.concatenate([x, [0.0, -0.0, 1.0 + 2.0 ** -8, 1.0 + 3 * 2.0 ** -8, 65504.0]])
+    ref = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).double().numpy()
+    assert np.array_equal(orc.bf16_round(x), ref)

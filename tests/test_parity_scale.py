@@ -76,7 +76,7 @@ def test_sampled_parity_at_scale(case, tmp_path):
     res = run_sampled(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
                           "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", str(d)],
                       env, tmp_path)
-    print(_ids(case), json.dumps({k: res[k] for k in ("O", "LSE", "dQ", "dK", "dV", "pin_lse", "pin_delta")
+    print(_ids(case), json.dumps({k: res[k] for k in ("O", "LSE", "dQ", "dK", "dV", "dK_vs_bf16ops", "dV_vs_bf16ops", "pin_lse", "pin_delta", "deviations")
                                   if k in res}))
     assert "LSE" in res and res["rows"] >= 512 and res["keys"] >= 256
     assert res["violations"] == [], res
