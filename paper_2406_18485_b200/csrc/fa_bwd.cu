@@ -33,6 +33,8 @@
 #include "sm100.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace a2d {
 
 // Optional wait-time instrumentation (build with -DA2D_PROFILE, see
@@ -63,12 +65,12 @@ __device__ unsigned long long g_bwd_prof[32];
 namespace bwd {
 constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 64;   // queries per iteration
-constexpr int QST = 3;   // Q/dO stages (TMA latency off the critical path)
+constexpr int kQstDefault = 3;  // Q/dO stages (TMA latency off the critical path)
 constexpr int kThreads = 512;
 constexpr int kMaxQTiles = 4096;                 // live-list capacity per launch (the C ABI slices longer query chunks)
 constexpr uint16_t kFullBit = 0x8000;
 // smem layout (bytes, from 1 KB aligned base) for head dim D (64 or 128)
-template <int D>
+template <int D, int QST = kQstDefault>
 struct Cfg {
   static constexpr int kK = 0;
   static constexpr int kV = kK + BK * D * 2;              // 32 KB each at D = 128
@@ -85,9 +87,10 @@ struct Cfg {
 };
 }  // namespace bwd
 
+template <int QST>
 struct BwdBars {
   uint64_t kv_full;
-  uint64_t qdo_full[bwd::QST], qdo_empty[bwd::QST];
+  uint64_t qdo_full[QST], qdo_empty[QST];
   uint64_t s_full[2], ds_full[2], dq_full[2], dq_empty[2], ds_free;
   uint64_t dkv_full;
   uint32_t tmem_base;
@@ -103,15 +106,17 @@ A2D_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
       : "memory");
 }
 
-template <int D>
+// D: head dim; QST: Q/dO pipeline stages; PF: L2 prefetch distance (in
+// iterations) of upcoming Q/dO tiles issued by the producer (0 = none).
+template <int D, int QST, int PF>
 __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_constant__ BwdParams p) {
   using namespace bwd;
-  using C = Cfg<D>;
+  using C = Cfg<D, QST>;
   constexpr int kK = C::kK, kV = C::kV, kQ = C::kQ, kDO = C::kDO, kDS = C::kDS, kDQ = C::kDQ;
   constexpr int kStats = C::kStats, kList = C::kList;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
-  __shared__ BwdBars bars;
+  __shared__ BwdBars<QST> bars;
 
   const int warp = warp_id(), lane = lane_id();
   const int nkt = (p.Tk + BK - 1) / BK;
@@ -203,11 +208,30 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tma_load_3d(smem + kV + c * 16384, &p.tm_v, &bars.kv_full, c * 64, key0, hk);
       }
       int it = 0;
+      if (PF > 0) {  // warm L2 with the first PF iterations' tiles
+        for (int j = 0; j < PF && j < n; ++j) {
+          const int qt = live_list[n_live - 1 - (j % n_live)] & (kFullBit - 1);
+          const int h = hk * p.G + j / n_live;
+          for (int c = 0; c < C::kPanels; ++c) {
+            tma_prefetch_l2_3d(&p.tm_q, c * 64, qt * BQ, h);
+            tma_prefetch_l2_3d(&p.tm_do, c * 64, qt * BQ, h);
+          }
+        }
+      }
       for (int g = 0; g < p.G; ++g) {
         const int h = hk * p.G + g;
         for (int li = 0; li < n_live; ++li, ++it) {
           const int qt = live_list[n_live - 1 - li] & (kFullBit - 1);
           const int qs = it % QST;
+          if (PF > 0 && it + PF < n) {  // L2 prefetch PF iterations ahead (no smem needed)
+            const int j = it + PF;
+            const int qtp = live_list[n_live - 1 - (j % n_live)] & (kFullBit - 1);
+            const int hp = hk * p.G + j / n_live;
+            for (int c = 0; c < C::kPanels; ++c) {
+              tma_prefetch_l2_3d(&p.tm_q, c * 64, qtp * BQ, hp);
+              tma_prefetch_l2_3d(&p.tm_do, c * 64, qtp * BQ, hp);
+            }
+          }
           PWAIT(&bars.qdo_empty[qs], ((it / QST) & 1) ^ 1, 0);
           mbar_expect_tx(&bars.qdo_full[qs], 2 * BQ * D * 2 + 2 * BQ * 4);
           for (int c = 0; c < C::kPanels; ++c) {
@@ -497,21 +521,39 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D>
+template <int D, int QST, int PF>
 static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
-  constexpr int bytes = bwd::Cfg<D>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(fa_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  constexpr int bytes = bwd::Cfg<D, QST>::kBytes;
+  cudaError_t e =
+      cudaFuncSetAttribute(fa_bwd_kernel<D, QST, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   dim3 grid((p.Tk + bwd::BK - 1) / bwd::BK, p.Hkv);
-  fa_bwd_kernel<D><<<grid, bwd::kThreads, bytes, s>>>(p);
+  fa_bwd_kernel<D, QST, PF><<<grid, bwd::kThreads, bytes, s>>>(p);
   return cudaGetLastError();
+}
+
+// Experiment switch (A2D_BWD_VARIANT, read once): 0 default (3 stages, no
+// prefetch), 1 = 2 stages, 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead.
+static int bwd_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("A2D_BWD_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
   if (head_dim != 128 && head_dim != 64) return cudaErrorInvalidValue;
   if (p.Tk <= 0 || p.Hkv <= 0) return cudaSuccess;
   if ((p.Tq + bwd::BQ - 1) / bwd::BQ > bwd::kMaxQTiles) return cudaErrorInvalidValue;
-  return head_dim == 128 ? launch_bwd_d<128>(p, s) : launch_bwd_d<64>(p, s);
+  if (head_dim == 64) return launch_bwd_d<64, 3, 0>(p, s);
+  switch (bwd_variant()) {
+    case 1: return launch_bwd_d<128, 2, 0>(p, s);
+    case 2: return launch_bwd_d<128, 3, 4>(p, s);
+    case 3: return launch_bwd_d<128, 3, 8>(p, s);
+    default: return launch_bwd_d<128, 3, 0>(p, s);
+  }
 }
 
 }  // namespace a2d

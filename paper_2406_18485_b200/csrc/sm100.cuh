@@ -117,6 +117,13 @@ A2D_DEV void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
       : "memory");
 }
 
+// Warm L2 with a tensor tile (no smem destination, no barrier).
+A2D_DEV void tma_prefetch_l2_3d(const CUtensorMap* m, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 // CTA-pair load: lands in THIS CTA's smem, completes bytes on the mbarrier at
 // `bar_cluster` (the leader CTA's barrier, from mapa_shared(bar, 0)).
 A2D_DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1, int c2) {

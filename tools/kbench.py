@@ -30,7 +30,7 @@ def fwd():
     K.fwd_chunk(q, k, v, plan, plan, bool(a.causal), scale, lse, None, out)
 fwd(); torch.cuda.synchronize()
 lse2, delta = K.bwd_preprocess(out, do, lse)
-dq = K.dq_acc_t(H, S, dev)
+dq = K.dq_acc_t(H, S, dev, D)
 dk = torch.empty(Hkv, S, D, device=dev); dv = torch.empty_like(dk)
 def bwd():
     K.bwd_chunk(q, k, v, do, plan, plan, lse2, delta, dq, dk, dv, False, bool(a.causal), scale)

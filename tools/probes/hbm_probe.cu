@@ -113,6 +113,39 @@ __global__ void __launch_bounds__(256) dqt_smem_kernel(const float* __restrict__
   }
 }
 
+// Z: registers -> bf16 -> swizzled smem [token][feature] -> full 256-byte
+// token rows to global (each warp store covers two whole rows).
+__global__ void __launch_bounds__(512) dqt_z_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                    long long T_pad) {
+  __shared__ __align__(16) uint4 tile[128][16];  // [token][16-byte chunk (8 features), swizzled]
+  const int h = blockIdx.y;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long t0 = (long long)blockIdx.x * 128;
+  const float* s = src + ((size_t)h * D + 8 * w) * T_pad + t0 + 4 * lane;
+  float4 r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = __ldcs(reinterpret_cast<const float4*>(s + (size_t)i * T_pad));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = j == 0 ? r[i].x : j == 1 ? r[i].y : j == 2 ? r[i].z : r[i].w;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]), p3 = __floats2bfloat162_rn(v[6], v[7]);
+    const int row = 4 * lane + j;
+    tile[row][w ^ (lane & 15)] = make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                                            *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {  // 2048 chunks / 512 threads
+    const int idx = k * 512 + threadIdx.x;
+    const int row = idx / 16, c = idx % 16;
+    const uint4 val = tile[row][c ^ ((row >> 2) & 15)];
+    *reinterpret_cast<uint4*>(dst + ((size_t)h * T + t0 + row) * D + 8 * c) = val;
+  }
+}
+
 template <class F>
 void timeit(const char* name, double bytes, F launch) {
   for (int i = 0; i < 3; ++i) launch();
@@ -163,6 +196,8 @@ int main() {
   timeit("dqt regs tpt=2", dqt_bytes, [&] { dqt_kernel<2><<<dim3(T / 256, H), 512>>>(acc, dq, T); });
   timeit("dqt regs tpt=4", dqt_bytes, [&] { dqt_kernel<4><<<dim3(T / 512, H), 512>>>(acc, dq, T); });
   timeit("dqt smem 64x128 swizzled", dqt_bytes, [&] { dqt_smem_kernel<<<dim3(T / 64, H), 256>>>(acc, dq, T); });
+  timeit("dqt Z regs->bf16 smem->full rows", dqt_bytes, [&] { dqt_z_kernel<<<dim3(T / 128, H), 512>>>(acc, dq, T); });
+  timeit("dqt regs tpt=1 (again)", dqt_bytes, [&] { dqt_kernel<1><<<dim3(T / 128, H), 512>>>(acc, dq, T); });
   timeit("copy f32->f32 (cudaMemcpy D2D ref)", rows * D * 8.0,
          [&] { cudaMemcpyAsync(acc + rows * D / 2, acc, rows * D * 2, cudaMemcpyDeviceToDevice); });
   return 0;
