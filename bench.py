@@ -388,8 +388,8 @@ def main():
     # ---------------- exposed communication: same step with every NCCL call
     # skipped (kernels and buffers identical), max over ranks
     exposed = None
-    if world > 1 and a.runtime == "python":
-        op.comm_enabled = False
+    if world > 1:
+        run.comm_enabled = False
         step()
         torch.cuda.synchronize()
         dist.barrier()
@@ -399,7 +399,7 @@ def main():
             step()
         c1.record()
         torch.cuda.synchronize()
-        op.comm_enabled = True
+        run.comm_enabled = True
         tc = torch.tensor([c0.elapsed_time(c1)], device=dev, dtype=torch.float64)
         dist.all_reduce(tc, op=dist.ReduceOp.MAX)
         t_comp = float(tc.item()) / a.steps

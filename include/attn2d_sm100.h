@@ -176,6 +176,11 @@ int a2d_bwd(void* ctx, const void* saved, const void* dout, void* dq, void* dk, 
  * return A2D_ECUDA / A2D_ETIMEOUT; the context then refuses further calls
  * and only a2d_ctx_destroy is valid. */
 int a2d_sync(void* ctx, void* stream, int64_t timeout_ms);
+/* Measurement only: enabled = 0 skips every NCCL call of the context (same
+ * kernels and buffers; receive buffers keep stale data), so a layer timed
+ * that way minus the normal layer is the exposed communication
+ * (ref timeline.py:152's definition). Results are garbage while disabled. */
+int a2d_ctx_set_comm(void* ctx, int32_t enabled);
 int a2d_ctx_destroy(void* ctx);
 /* Host-side plan of the native runtime, exposed for tests and other hosts:
  * CP rank j's ring schedule as (source, outer step, inner step) triples

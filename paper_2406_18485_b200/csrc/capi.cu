@@ -86,7 +86,7 @@ int make_tmap_bf16_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t 
 // fp32 [n2][n1][n0] tensor map (row stride s1, plane stride s2 elements), box
 // {box0, box1, 1}, SWIZZLE_128B (box0 = 32): the transposed dQ reduce target.
 static int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uint64_t n1, uint64_t n2,
-                            uint64_t s1, uint64_t s2, uint32_t box0, uint32_t box1) {
+                            uint64_t s1, uint64_t s2, uint32_t box0, uint32_t box1, bool sw128 = true) {
   auto enc = get_encode();
   if (!enc) return fail(A2D_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(A2D_EINVAL, "tensor base not 16-byte aligned");
@@ -95,7 +95,8 @@ static int make_tmap_f32_3d(CUtensorMap* out, const void* base, uint64_t n0, uin
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(A2D_ECUDA, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string((int)r) + ")");
   return A2D_OK;
@@ -195,10 +196,10 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
     return fail(A2D_EINVAL, std::to_string(H) + " query heads not divisible by " + std::to_string(H_kv) + " kv heads");
   if (Tq < 0 || Tk < 0 || Tq > INT32_MAX / 2 || Tk > INT32_MAX / 2) return fail(A2D_EINVAL, "a2d_fa_bwd_chunk: bad T");
   if (Tk == 0) return A2D_OK;
-  // One launch covers at most 4096 query tiles (256K rows: the kernel's
+  // One launch covers at most 2048 query tiles (128K rows: the kernel's
   // shared-memory live list); longer query chunks run as consecutive slices,
   // later slices accumulating into dk/dv.
-  constexpr int64_t kSlice = 4096 * 64;
+  constexpr int64_t kSlice = 2048 * 64;
   const int tq_pad = (int)((Tq + 63) / 64 * 64);
   for (int64_t off = 0; off < (Tq > 0 ? Tq : 1); off += kSlice) {
     const int64_t len = Tq > 0 ? std::min(kSlice, Tq - off) : 0;
@@ -214,10 +215,13 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
       // dq_acc^T [H][D][tq_pad]: this slice starts at query `off`
       if ((rc = make_tmap_f32_3d(&p.tm_dq, dq_acc + off, len, D, H, tq_pad, (uint64_t)D * tq_pad, 32, D)))
         return rc;
+      if ((rc = make_tmap_f32_3d(&p.tm_dq8, dq_acc + off, len, D, H, tq_pad, (uint64_t)D * tq_pad, 8, 32, false)))
+        return rc;
     } else {
       p.tm_q = p.tm_k;
       p.tm_do = p.tm_k;
       p.tm_dq = p.tm_k;
+      p.tm_dq8 = p.tm_k;
     }
     p.q_pos = q_pos + off;
     p.k_pos = k_pos;

@@ -67,10 +67,13 @@ constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 64;   // queries per iteration
 constexpr int kQstDefault = 3;  // Q/dO stages (TMA latency off the critical path)
 constexpr int kThreads = 512;
-constexpr int kMaxQTiles = 4096;                 // live-list capacity per launch (the C ABI slices longer query chunks)
+constexpr int kMaxQTiles = 2048;                 // live-list capacity per launch (the C ABI slices longer query chunks)
 constexpr uint16_t kFullBit = 0x8000;
 // smem layout (bytes, from 1 KB aligned base) for head dim D (64 or 128)
-template <int D, int QST = kQstDefault>
+// DQ8: per-warp dQ drain in 8-query chunks through 2 x 1 KB staging buffers
+// per warp (8 KB in all instead of 32 KB), which is what makes room for a 4th
+// Q/dO stage.
+template <int D, int QST = kQstDefault, bool DQ8 = false>
 struct Cfg {
   static constexpr int kK = 0;
   static constexpr int kV = kK + BK * D * 2;              // 32 KB each at D = 128
@@ -78,7 +81,7 @@ struct Cfg {
   static constexpr int kDO = kQ + QST * BQ * D * 2;       // QST x 16 KB
   static constexpr int kDS = kDO + QST * BQ * D * 2;      // 16 KB  (dS^T, [key][q] SW128)
   static constexpr int kDQ = kDS + BK * BQ * 2;           // fp32 dQ staging: 2 SW128 boxes [D][32 q]
-  static constexpr int kStats = kDQ + BQ * D * 4;         // QST x (lse2[64], delta[64])
+  static constexpr int kStats = kDQ + (DQ8 ? 4 * 2 * 1024 : BQ * D * 4);  // QST x (lse2[64], delta[64])
   static constexpr int kList = kStats + QST * 2 * BQ * 4; // live query tiles (uint16)
   static constexpr int kEnd = kList + kMaxQTiles * 2;
   static constexpr int kBytes = kEnd + 1024;
@@ -108,10 +111,10 @@ A2D_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 
 // D: head dim; QST: Q/dO pipeline stages; PF: L2 prefetch distance (in
 // iterations) of upcoming Q/dO tiles issued by the producer (0 = none).
-template <int D, int QST, int PF>
+template <int D, int QST, int PF, bool DQ8>
 __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_constant__ BwdParams p) {
   using namespace bwd;
-  using C = Cfg<D, QST>;
+  using C = Cfg<D, QST, DQ8>;
   constexpr int kK = C::kK, kV = C::kV, kQ = C::kQ, kDO = C::kDO, kDS = C::kDS, kDQ = C::kDQ;
   constexpr int kStats = C::kStats, kList = C::kList;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   if (warp == 2) tmem_alloc<512>(&bars.tmem_base);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.tm_q); tma_prefetch(&p.tm_k); tma_prefetch(&p.tm_v); tma_prefetch(&p.tm_do);
-    tma_prefetch(&p.tm_dq);
+    tma_prefetch(DQ8 ? &p.tm_dq8 : &p.tm_dq);
   }
   // ---- compacted list of live query tiles: every warp scans a contiguous
   // range, counts, then writes its survivors at its prefix offset.
@@ -268,7 +271,9 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       const uint64_t dKmn = sdesc_sw128(sK, 16384, 1024);  // K as MN-major A of dQ^T
       const uint64_t dDSmn = sdesc_sw128(sDS, 8192, 1024);  // dS^T as MN-major B of dQ^T
       const uint64_t dQmn = sdesc_sw128(sQ, 8192, 1024), dDOmn = sdesc_sw128(sDO, 8192, 1024);
-      auto issue_s = [&](int i) {  // S^T_i and dP^T_i into region i&1, then commit s_full
+      // S^T_i and dP^T_i (part 0: both, interleaved per K step) into region
+      // i&1, then commit s_full.
+      auto issue_s = [&](int i, int part) {
         const int b = i & 1, qs = i % QST;
         const uint32_t tS = tmem + b * 128, tDP = tmem + b * 128 + 64;
         const uint64_t qoff = (uint64_t)((qs * BQ * D * 2) >> 4);
@@ -278,10 +283,10 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
           for (int k = 0; k < D / 16; ++k) {
             const uint64_t ka = (uint64_t)(((k / 4) * 16384 + (k % 4) * 32) >> 4);
             const uint64_t kq = qoff + (uint64_t)(((k / 4) * 8192 + (k % 4) * 32) >> 4);
-            umma_ss(tS, dK0 + ka, dQ0 + kq, id_s, k > 0);
-            umma_ss(tDP, dV0 + ka, dDO0 + kq, id_s, k > 0);
+            if (part != 2) umma_ss(tS, dK0 + ka, dQ0 + kq, id_s, k > 0);
+            if (part != 1) umma_ss(tDP, dV0 + ka, dDO0 + kq, id_s, k > 0);
           }
-          umma_commit(&bars.s_full[b]);
+          if (part != 1) umma_commit(&bars.s_full[b]);
         }
         __syncwarp();
       };
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
       for (int i = 0; i < 2 && i < n; ++i) {
         PWAIT(&bars.qdo_full[i % QST], (i / QST) & 1, 1);
         tc_fence_after();
-        issue_s(i);
+        issue_s(i, 0);
       }
       for (int i = 0; i < n; ++i) {
         const int b = i & 1, qs = i % QST;
@@ -318,10 +323,12 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         }
         __syncwarp();
         if (i + 2 < n) {
+          // (r02: issuing S^T_{i+2} before the dq_empty wait measured 4% slower —
+          // it exposes the Q/dO TMA latency the drain wait used to cover)
           PWAIT(&bars.dq_empty[b], (i >> 1) & 1, 3);
           PWAIT(&bars.qdo_full[(i + 2) % QST], ((i + 2) / QST) & 1, 1);
           tc_fence_after();
-          issue_s(i + 2);
+          issue_s(i + 2, 0);
         }
       }
       __syncwarp();
@@ -356,6 +363,39 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars.dq_empty[b]);
+        if constexpr (DQ8) {
+          // Each warp drains its own 32 features independently: 8 chunks of 8
+          // queries, [32 d][8 q] fp32 (1 KB) through two alternating buffers,
+          // one TMA reduce-add per chunk (box {8 q, 32 d}); no cross-warp barrier.
+          if (wq * 32 < D) {
+            float* wbuf = dq_stage + wq * 512;  // 2 x 256 floats per warp
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              float* buf = wbuf + (c & 1) * 256;
+#ifdef A2D_PROFILE
+              const long long tr0 = clock64();
+#endif
+              if (lane == 0) bulk_wait_read1();  // the reduce that read `buf` two chunks ago is done
+#ifdef A2D_PROFILE
+              prof[1] += clock64() - tr0;
+#endif
+              __syncwarp();
+              const uint32_t* src = c < 4 ? v0 + 8 * c : v1 + 8 * (c - 4);
+              float4* dst = reinterpret_cast<float4*>(buf + lane * 8);
+              dst[0] = make_float4(__uint_as_float(src[0]) * scale, __uint_as_float(src[1]) * scale,
+                                   __uint_as_float(src[2]) * scale, __uint_as_float(src[3]) * scale);
+              dst[1] = make_float4(__uint_as_float(src[4]) * scale, __uint_as_float(src[5]) * scale,
+                                   __uint_as_float(src[6]) * scale, __uint_as_float(src[7]) * scale);
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_reduce_add_3d(&p.tm_dq8, buf, qt * BQ + 8 * c, wq * 32, h);
+                bulk_commit();
+              }
+            }
+          }
+          continue;
+        }
 #ifdef A2D_PROFILE
         const long long tr0 = clock64();
 #endif
@@ -388,7 +428,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
         }
       }
     }
-    if (leader) bulk_wait0();
+    if (DQ8 ? lane == 0 : leader) bulk_wait0();
     if (warp == 12) PFLUSH(2);
   } else if (warp >= 4) {
     // ------------------------------------------------ P/dS warpgroups
@@ -521,19 +561,21 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D, int QST, int PF>
+template <int D, int QST, int PF, bool DQ8 = false>
 static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
-  constexpr int bytes = bwd::Cfg<D, QST>::kBytes;
+  constexpr int bytes = bwd::Cfg<D, QST, DQ8>::kBytes;
+  static_assert(bytes <= 232448, "backward shared memory exceeds 227 KB");
   cudaError_t e =
-      cudaFuncSetAttribute(fa_bwd_kernel<D, QST, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(fa_bwd_kernel<D, QST, PF, DQ8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   dim3 grid((p.Tk + bwd::BK - 1) / bwd::BK, p.Hkv);
-  fa_bwd_kernel<D, QST, PF><<<grid, bwd::kThreads, bytes, s>>>(p);
+  fa_bwd_kernel<D, QST, PF, DQ8><<<grid, bwd::kThreads, bytes, s>>>(p);
   return cudaGetLastError();
 }
 
 // Experiment switch (A2D_BWD_VARIANT, read once): 0 default (3 stages, no
-// prefetch), 1 = 2 stages, 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead.
+// prefetch), 1 = 2 stages, 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead,
+// 4 = 4 stages with the per-warp 8-query dQ drain, 5 = 3 stages with it.
 static int bwd_variant() {
   static int v = -1;
   if (v < 0) {
@@ -552,6 +594,8 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
     case 1: return launch_bwd_d<128, 2, 0>(p, s);
     case 2: return launch_bwd_d<128, 3, 4>(p, s);
     case 3: return launch_bwd_d<128, 3, 8>(p, s);
+    case 4: return launch_bwd_d<128, 4, 0, true>(p, s);
+    case 5: return launch_bwd_d<128, 3, 0, true>(p, s);
     default: return launch_bwd_d<128, 3, 0>(p, s);
   }
 }

@@ -28,6 +28,30 @@
 
 namespace a2d {
 
+// Optional wait-time instrumentation (-DA2D_PROFILE, build.py --profile):
+// g_fwd_prof[role*8 + slot], role 0 MMA warp, 1 softmax WG0 (warp 4 lane 0),
+// 2 softmax WG1 (warp 8 lane 0), 3 TMA producer; slot 7 = role's total cycles.
+#ifdef A2D_PROFILE
+__device__ unsigned long long g_fwd_prof[32];
+#define FWAIT(bar, ph, slot)         \
+  do {                               \
+    const long long t0_ = clock64(); \
+    mbar_wait(bar, ph);              \
+    prof[slot] += clock64() - t0_;   \
+  } while (0)
+#define FSTART() const long long pt0_ = clock64()
+#define FFLUSH(role)                                                                              \
+  do {                                                                                            \
+    prof[7] = clock64() - pt0_;                                                                   \
+    if (lane == 0)                                                                                \
+      for (int s_ = 0; s_ < 8; ++s_) atomicAdd(&g_fwd_prof[(role) * 8 + s_], (unsigned long long)prof[s_]); \
+  } while (0)
+#else
+#define FWAIT(bar, ph, slot) mbar_wait(bar, ph)
+#define FSTART()
+#define FFLUSH(role)
+#endif
+
 namespace fwd {
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 384;
@@ -220,8 +244,11 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
   const int n = bars.n_live;
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  (void)prof;
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    FSTART();
     if (lane == 0 && n > 0) {
       mbar_expect_tx(&bars.q_full, 2 * L::kTileBytes);
       for (int t = 0; t < 2; ++t)
@@ -231,22 +258,24 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       for (int it = 0; it < n; ++it) {
         const int j = live_list[it] & kIdx;
         const int ks = it % KST, kph = (it / KST) & 1;
-        mbar_wait(&bars.k_empty[ks], kph ^ 1);
+        FWAIT(&bars.k_empty[ks], kph ^ 1, 0);
         mbar_expect_tx(&bars.k_full[ks], L::kTileBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_3d(smem + L::kK + ks * L::kTileBytes + c * 16384, &p.tm_k, &bars.k_full[ks], c * 64,
                       j * BN, hk);
         const int vs = it % VST, vph = (it / VST) & 1;
-        mbar_wait(&bars.v_empty[vs], vph ^ 1);
+        FWAIT(&bars.v_empty[vs], vph ^ 1, 1);
         mbar_expect_tx(&bars.v_full[vs], L::kTileBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_3d(smem + L::kV + vs * L::kTileBytes + c * 16384, &p.tm_v, &bars.v_full[vs], c * 64,
                       j * BN, hk);
       }
     }
+    FFLUSH(3);
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // Converged warp (uniform-register descriptors); an elected lane issues.
+    FSTART();
     if (n > 0) {
       constexpr uint32_t id_qk = idesc_bf16(BM, BN, false, false);
       constexpr uint32_t id_pv = idesc_bf16(BM, D, false, true);
@@ -283,11 +312,11 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       __syncwarp();
       for (int it = 0; it < n; ++it) {
         const int vs = it % VST;
-        mbar_wait(&bars.v_full[vs], (it / VST) & 1);
+        FWAIT(&bars.v_full[vs], (it / VST) & 1, 0);
         const bool more = it + 1 < n;
         const int ks1 = (it + 1) % KST;
-        mbar_wait(&bars.p_full[0], it & 1);
-        if (more) mbar_wait(&bars.k_full[ks1], ((it + 1) / KST) & 1);
+        FWAIT(&bars.p_full[0], it & 1, 1);
+        if (more) FWAIT(&bars.k_full[ks1], ((it + 1) / KST) & 1, 2);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
@@ -300,7 +329,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           }
         }
         __syncwarp();
-        mbar_wait(&bars.p_full[1], it & 1);
+        FWAIT(&bars.p_full[1], it & 1, 3);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
@@ -317,6 +346,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         __syncwarp();
       }
     }
+    FFLUSH(0);
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax
     const int t = (warp - 4) / 4;          // query tile of this warpgroup
@@ -332,12 +362,13 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
 
     float m_used = -INFINITY;  // running max, log2 units (scaled)
     float l_sum = 0.f;
+    FSTART();
     for (int it = 0; it < n; ++it) {
       const int ent = live_list[it];
       const int j = ent & kIdx;
       const bool full = (ent & (t == 0 ? kMask0 : kMask1)) == 0;
 
-      mbar_wait(&bars.s_full[t], it & 1);
+      FWAIT(&bars.s_full[t], it & 1, 0);
       tc_fence_after();
       float s[BN];
       {
@@ -366,16 +397,19 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           s[c] = keep ? s[c] : -INFINITY;
         }
       }
-      // row max: four independent chains (short dependency depth)
-      float mq[4] = {s[0], s[1], s[2], s[3]};
+      // row max: four independent chains of three-input max (FMNMX3)
+      static_assert(BN % 8 == 0 && BN >= 16, "row max tiling");
+      float mq[4];
 #pragma unroll
-      for (int c = 4; c < BN; c += 4) {
-        mq[0] = fmaxf(mq[0], s[c]);
-        mq[1] = fmaxf(mq[1], s[c + 1]);
-        mq[2] = fmaxf(mq[2], s[c + 2]);
-        mq[3] = fmaxf(mq[3], s[c + 3]);
+      for (int k = 0; k < 4; ++k) mq[k] = fmax3(s[k], s[k + 4], s[k + 8]);  // columns 0..11
+#pragma unroll
+      for (int c = 12; c + 8 <= BN - 4; c += 8) {                           // 12 .. BN-5
+        mq[0] = fmax3(mq[0], s[c], s[c + 4]);
+        mq[1] = fmax3(mq[1], s[c + 1], s[c + 5]);
+        mq[2] = fmax3(mq[2], s[c + 2], s[c + 6]);
+        mq[3] = fmax3(mq[3], s[c + 3], s[c + 7]);
       }
-      const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+      const float mx = fmaxf(fmax3(mq[0], mq[1], s[BN - 4]), fmax3(mq[2], mq[3], fmax3(s[BN - 3], s[BN - 2], s[BN - 1])));
       const float m_tile = mx * sl2;  // -inf stays -inf (sl2 > 0)
       float alpha = 1.f;
       bool rescale = false;
@@ -429,6 +463,8 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       mbar_arrive(&bars.p_full[t]);
     }
 
+    if (warp == 4) FFLUSH(1);
+    if (warp == 8) FFLUSH(2);
     // ---------------------------------------------------------- epilogue
     const int it = n;
     if (it > 0) {
@@ -463,3 +499,12 @@ cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s) {
 }
 
 }  // namespace a2d
+
+#ifdef A2D_PROFILE
+extern "C" int a2d_prof_read_fwd(unsigned long long* out, int n) {
+  if (n > 32) n = 32;
+  if (cudaMemcpyFromSymbol(out, a2d::g_fwd_prof, n * sizeof(unsigned long long)) != cudaSuccess) return 2;
+  unsigned long long z[32] = {0};
+  return cudaMemcpyToSymbol(a2d::g_fwd_prof, z, sizeof(z)) == cudaSuccess ? 0 : 2;
+}
+#endif

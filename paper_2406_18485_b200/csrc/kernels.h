@@ -31,7 +31,8 @@ cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s);
 // D = rowsum(dO * O) of the query chunk.
 struct BwdParams {
   CUtensorMap tm_q, tm_k, tm_v, tm_do;  // box {64,64,1} for q/do, {64,128,1} for k/v
-  CUtensorMap tm_dq;                    // fp32 dq_acc^T [H][128][Tq_pad], box {32 q,128 d,1}, SW128
+  CUtensorMap tm_dq;                    // fp32 dq_acc^T [H][D][Tq_pad], box {32 q,D d,1}, SW128
+  CUtensorMap tm_dq8;                   // same tensor, box {8 q,32 d,1}, no swizzle (per-warp drain)
   const int* q_pos;
   const int* k_pos;
   const int2* q_bounds;   // per 64-row query tile

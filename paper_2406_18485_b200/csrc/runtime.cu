@@ -65,6 +65,7 @@ struct Ctx {
   float* g32_sum = nullptr;
   void* dkv_home = nullptr;
   size_t off_kv = 0, off_out = 0, off_lse = 0, saved_bytes = 0;  // Saved layout
+  bool comm = true;  // false: every NCCL call skipped (same kernels / buffers) — exposed-comm measurement only
 };
 
 // One forward's state inside the caller's saved buffer (256-byte aligned
@@ -127,6 +128,7 @@ void ring_plan(int d_cp, int w, int j, std::vector<Step>* steps, int peers[6]) {
 
 // grouped send/recv of bytes_per_peer to/from every member of the HP group
 int a2a(Ctx& c, const void* send, void* recv, size_t bytes_per_peer, cudaStream_t s) {
+  if (!c.comm) return A2D_OK;
   NCCL_TRY(ncclGroupStart());
   for (int p = 0; p < c.d_hp; ++p) {
     NCCL_TRY(ncclSend(static_cast<const char*>(send) + p * bytes_per_peer, bytes_per_peer, ncclUint8, p, c.hp_comm, s));
@@ -141,10 +143,12 @@ int hop(Ctx& c, ncclComm_t comm, cudaStream_t side, cudaStream_t main, const voi
         size_t bytes, cudaEvent_t done) {
   CUDA_TRY(cudaEventRecord(c.ev_ready, main));
   CUDA_TRY(cudaStreamWaitEvent(side, c.ev_ready, 0));
-  NCCL_TRY(ncclGroupStart());
-  NCCL_TRY(ncclSend(send, bytes, ncclUint8, to, comm, side));
-  NCCL_TRY(ncclRecv(recv, bytes, ncclUint8, from, comm, side));
-  NCCL_TRY(ncclGroupEnd());
+  if (c.comm) {
+    NCCL_TRY(ncclGroupStart());
+    NCCL_TRY(ncclSend(send, bytes, ncclUint8, to, comm, side));
+    NCCL_TRY(ncclRecv(recv, bytes, ncclUint8, from, comm, side));
+    NCCL_TRY(ncclGroupEnd());
+  }
   CUDA_TRY(cudaEventRecord(done, side));
   return A2D_OK;
 }
@@ -545,6 +549,12 @@ int a2d_bwd(void* ctx, const void* saved, const void* dout, void* dq, void* dk, 
   Ctx& c = *static_cast<Ctx*>(ctx);
   if (!c.world_comm) return set_error(A2D_EINVAL, "a2d_bwd: context was aborted");
   return backward(c, saved, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+}
+
+int a2d_ctx_set_comm(void* ctx, int32_t enabled) {
+  if (!ctx) return set_error(A2D_EINVAL, "a2d_ctx_set_comm: null context");
+  static_cast<Ctx*>(ctx)->comm = enabled != 0;
+  return A2D_OK;
 }
 
 int a2d_sync(void* ctx, void* stream, int64_t timeout_ms) {

@@ -17,7 +17,7 @@ BF16 = torch.bfloat16
 FWD_DIMS = (64, 128)
 BWD_DIMS = (64, 128)
 BWD_DIM = 128  # the native runtime's head dim
-BWD_QSLICE = 4096 * 64  # query rows per fa_bwd launch (capi.cu a2d_fa_bwd_chunk)
+BWD_QSLICE = 2048 * 64  # query rows per fa_bwd launch (capi.cu a2d_fa_bwd_chunk)
 
 
 def _stream() -> int:

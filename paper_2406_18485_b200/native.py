@@ -77,6 +77,16 @@ class NativeAttn2D:
                   dv.data_ptr(), torch.cuda.current_stream().cuda_stream)
         return dq, dk, dv
 
+    @property
+    def comm_enabled(self) -> bool:
+        return getattr(self, "_comm", True)
+
+    @comm_enabled.setter
+    def comm_enabled(self, on: bool) -> None:
+        """Measurement only (exposed communication): False skips every NCCL call."""
+        self._comm = bool(on)
+        _lib.call("a2d_ctx_set_comm", self._ctx, int(self._comm))
+
     def sync(self, timeout_s: float = 600.0) -> None:
         """Wait for this rank's queued layer work, polling NCCL for asynchronous
         errors; raises (and aborts the communicators) on an error or timeout."""

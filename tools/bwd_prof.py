@@ -29,6 +29,12 @@ SLOTS = {
     "drain": ["dq_full(dQ GEMM)", "bulk_wait_read(TMA reduce)", "-", "-", "-", "-", "-", "total"],
     "tma": ["qdo_empty(MMA frees stage)", "-", "-", "-", "-", "-", "-", "total"],
 }
+FWD_SLOTS = {
+    "mma": ["v_full(TMA)", "p_full0(softmax WG0)", "k_full(TMA)", "p_full1(softmax WG1)", "-", "-", "-", "total"],
+    "softmax0": ["s_full(MMA QK)", "-", "-", "-", "-", "-", "-", "total"],
+    "softmax1": ["s_full(MMA QK)", "-", "-", "-", "-", "-", "-", "total"],
+    "tma": ["k_empty", "v_empty", "-", "-", "-", "-", "-", "total"],
+}
 
 
 def main():
@@ -37,9 +43,11 @@ def main():
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=32)
     ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--pass", dest="which", default="bwd", choices=["bwd", "fwd"])
     a = ap.parse_args()
     lib = _lib.load(os.environ["A2D_LIB"])
     lib.a2d_prof_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.a2d_prof_read_fwd.argtypes = [ctypes.c_void_p, ctypes.c_int]
     dev = torch.device("cuda:0")
     H, Hkv, S, d = a.heads, a.kv_heads, a.seq, a.dim
     g = torch.Generator(device=dev).manual_seed(0)
@@ -55,6 +63,24 @@ def main():
     dk = torch.empty((Hkv, S, d), dtype=torch.float32, device=dev)
     dv = torch.empty_like(dk)
     buf = (ctypes.c_ulonglong * 32)()
+    if a.which == "fwd":
+        torch.cuda.synchronize()
+        lib.a2d_prof_read_fwd(buf, 32)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        K.fwd_chunk(q, k, v, plan, plan, True, scale, lse, None, out)
+        e1.record()
+        torch.cuda.synchronize()
+        lib.a2d_prof_read_fwd(buf, 32)
+        ms = e0.elapsed_time(e1)
+        res = {"shape": vars(a), "fwd_ms": ms, "fwd_tflops": 2.0 * S * S * H * d / ms / 1e9}
+        for role, base in (("mma", 0), ("softmax0", 8), ("softmax1", 16), ("tma", 24)):
+            vals = list(buf[base:base + 8])
+            tot = vals[7] or 1
+            res[role] = {FWD_SLOTS[role][i]: round(vals[i] / tot, 4) for i in range(7) if FWD_SLOTS[role][i] != "-"}
+            res[role]["total_Gcycles"] = vals[7] / 1e9
+        print(json.dumps(res, indent=1))
+        return
     K.bwd_chunk(q, k, v, do, plan, plan, lse2, delta, dq_acc, dk, dv, False, True, scale)  # warm-up
     torch.cuda.synchronize()
     lib.a2d_prof_read(buf, 32)
