@@ -230,6 +230,53 @@ def hbm_roofline(events, peak_gbs: float) -> dict:
     return out
 
 
+def hbm_isolated(H: int, C: int, d: int, dev, peak_gbs: float, reps: int = 5) -> dict:
+    """Each HBM-bound kernel of the path timed ALONE (CUDA events, `reps`
+    back-to-back launches after a warm-up) on tensors of this rank's bench
+    sizes: (H, C, d) bf16 activations, the fp32 transposed dQ accumulator,
+    fp32 dK/dV-sized buffers. Complements the in-step `hbm_roofline`, whose
+    kernels run at the power-capped clock of the attention step."""
+    import torch
+
+    from paper_2406_18485_b200 import kernels as K
+    g = torch.Generator(device=dev).manual_seed(5)
+    o = torch.randn((H, C, d), device=dev, generator=g).to(torch.bfloat16)
+    do = torch.randn((H, C, d), device=dev, generator=g).to(torch.bfloat16)
+    lse = torch.randn((H, C), device=dev, generator=g)
+    acc = torch.randn((H, d, (C + 63) // 64 * 64), device=dev, generator=g)
+    f32a = torch.randn((H, C, d), device=dev, generator=g)
+    f32b = torch.randn((H, C, d), device=dev, generator=g)
+    lse_b = torch.randn((H, C), device=dev, generator=g)
+    idx = torch.arange(H, dtype=torch.int32, device=dev).flip(0)
+    dst = torch.empty_like(o)
+    a_hp = 4 if H % 4 == 0 else 1
+    cases = {
+        "a2d_bwd_preprocess": (lambda: K.bwd_preprocess(o, do, lse), H * C * (4 * d + 4) + H * ((C + 63) // 64 * 64) * 8),
+        "a2d_dqt_to_bf16": (lambda: K.dqt_to_bf16(acc, C), H * C * d * 6),
+        "a2d_gather_blocks": (lambda: K.gather_blocks(o, idx, dst), 2 * o.numel() * 2),
+        "a2d_permute_blocks": (lambda: K.permute_blocks(o, a_hp, H // a_hp, out=dst), 2 * o.numel() * 2),
+        "a2d_permute_f32_to_bf16": (lambda: K.permute_to_bf16(f32a, a_hp, H // a_hp, out=dst), 6 * f32a.numel()),
+        "a2d_add_f32": (lambda: K.add_(f32a, f32b), 12 * f32a.numel()),
+        "a2d_merge": (lambda: K.merge_(f32a, lse, f32b, lse_b), H * C * (12 * d + 12)),
+    }
+    out = {}
+    for name, (fn, nbytes) in cases.items():
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"bytes": nbytes, "ms": ms, "gbs": gbs, "peak": peak_gbs, "frac": gbs / peak_gbs}
+    del o, do, acc, f32a, f32b, dst
+    torch.cuda.empty_cache()
+    return out
+
+
 def parity_check(a, run, op, q, k, v, do, world, rank):
     """Sampled f64-oracle parity of one step of the benched configuration on
     the benched inputs (oracle/sampled.py; checker only, outside every timed
@@ -483,6 +530,12 @@ def main():
                "pipelining": "side copy stream: H2D of step i+1 and D2H of step i overlap step i+1 compute; "
                               "dO's H2D overlaps the forward of its own step"}
 
+    hbm_iso = None
+    if rank == 0:
+        try:
+            hbm_iso = hbm_isolated(op.Hl, op.C, op.kd, dev, peaks()["hbm_gbs"])
+        except Exception as exc:
+            hbm_iso = {"error": f"{type(exc).__name__}: {exc}"}
     parity = None
     if a.check:
         try:
@@ -532,7 +585,8 @@ def main():
             "mfu_sustained": per_gpu / pk["bf16_tflops_sustained"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / a.steps,
-            "clocks": clk, "exposed_comm": exposed, "hbm_roofline": hbm, "parity": parity,
+            "clocks": clk, "exposed_comm": exposed, "hbm_roofline": hbm,
+            "hbm_roofline_isolated": hbm_iso, "parity": parity,
         }
         print(json.dumps(line))
     dist.barrier()

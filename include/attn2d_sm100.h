@@ -181,6 +181,11 @@ int a2d_sync(void* ctx, void* stream, int64_t timeout_ms);
  * that way minus the normal layer is the exposed communication
  * (ref timeline.py:152's definition). Results are garbage while disabled. */
 int a2d_ctx_set_comm(void* ctx, int32_t enabled);
+/* Head-parallel exchange transport the context chose at creation: 1 = copy
+ * engines into CUDA-IPC-mapped peer buffers plus an NCCL barrier (default when
+ * every HP peer could map the others), 0 = NCCL send/recv (A2D_TRANSPORT=nccl,
+ * or any rank failed to map). Ring hops always use NCCL. */
+int a2d_ctx_transport(void* ctx, int32_t* symm);
 int a2d_ctx_destroy(void* ctx);
 /* Host-side plan of the native runtime, exposed for tests and other hosts:
  * CP rank j's ring schedule as (source, outer step, inner step) triples

@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <thread>
 #include <cmath>
@@ -66,6 +67,20 @@ struct Ctx {
   void* dkv_home = nullptr;
   size_t off_kv = 0, off_out = 0, off_lse = 0, saved_bytes = 0;  // Saved layout
   bool comm = true;  // false: every NCCL call skipped (same kernels / buffers) — exposed-comm measurement only
+  // copy-engine head-parallel exchange ("symm"): every HP rank's exchange
+  // buffer is IPC-mapped into its peers; a rank writes the chunk for peer p
+  // straight into p's buffer with cudaMemcpyAsync (no SMs), then a tiny NCCL
+  // all-reduce on the HP communicator is the barrier after which every
+  // incoming chunk has landed. IN region: q + kv (fwd) / dO (bwd); OUT: out /
+  // dq + dk + dv; consecutive uses of one region are always separated by an
+  // exchange (hence a barrier) on the other, so no extra handshake is needed.
+  bool symm = false;
+  char* xbuf = nullptr;
+  size_t x_in = 0, x_out = 0;
+  std::vector<char*> xpeer;  // [d_hp]: peers' mapped buffers (own = xbuf)
+  std::vector<cudaStream_t> xs;
+  std::vector<cudaEvent_t> xe;
+  int* xflag = nullptr;
 };
 
 // One forward's state inside the caller's saved buffer (256-byte aligned
@@ -126,8 +141,34 @@ void ring_plan(int d_cp, int w, int j, std::vector<Step>* steps, int peers[6]) {
   std::copy(v, v + 6, peers);
 }
 
-// grouped send/recv of bytes_per_peer to/from every member of the HP group
-int a2a(Ctx& c, const void* send, void* recv, size_t bytes_per_peer, cudaStream_t s) {
+// All-to-all of bytes_per_peer between the members of the HP group: chunk p
+// of `send` goes to peer p; peer p's chunk for this rank lands at position p.
+// NCCL transport: grouped ncclSend/ncclRecv into `recv`. Copy-engine
+// transport: into the exchange buffer at byte offset `off` (returned via
+// *landed; `recv` is not touched).
+int a2a(Ctx& c, const void* send, void* recv, size_t bytes_per_peer, cudaStream_t s, size_t off = 0,
+        const void** landed = nullptr) {
+  if (landed) *landed = recv;
+  if (c.symm) {
+    char* dst0 = c.xbuf + off;
+    if (landed) *landed = dst0;
+    if (!c.comm) return A2D_OK;
+    CUDA_TRY(cudaEventRecord(c.ev_ready, s));
+    for (int i = 0; i < c.d_hp - 1; ++i) {
+      const int p = (c.hp + 1 + i) % c.d_hp;
+      CUDA_TRY(cudaStreamWaitEvent(c.xs[i], c.ev_ready, 0));
+      CUDA_TRY(cudaMemcpyAsync(c.xpeer[p] + off + (size_t)c.hp * bytes_per_peer,
+                               static_cast<const char*>(send) + (size_t)p * bytes_per_peer, bytes_per_peer,
+                               cudaMemcpyDeviceToDevice, c.xs[i]));
+      CUDA_TRY(cudaEventRecord(c.xe[i], c.xs[i]));
+    }
+    CUDA_TRY(cudaMemcpyAsync(dst0 + (size_t)c.hp * bytes_per_peer,
+                             static_cast<const char*>(send) + (size_t)c.hp * bytes_per_peer, bytes_per_peer,
+                             cudaMemcpyDeviceToDevice, s));
+    for (int i = 0; i < c.d_hp - 1; ++i) CUDA_TRY(cudaStreamWaitEvent(s, c.xe[i], 0));
+    NCCL_TRY(ncclAllReduce(c.xflag, c.xflag, 1, ncclInt32, ncclSum, c.hp_comm, s));  // barrier: all chunks landed
+    return A2D_OK;
+  }
   if (!c.comm) return A2D_OK;
   NCCL_TRY(ncclGroupStart());
   for (int p = 0; p < c.d_hp; ++p) {
@@ -135,6 +176,16 @@ int a2a(Ctx& c, const void* send, void* recv, size_t bytes_per_peer, cudaStream_
     NCCL_TRY(ncclRecv(static_cast<char*>(recv) + p * bytes_per_peer, bytes_per_peer, ncclUint8, p, c.hp_comm, s));
   }
   NCCL_TRY(ncclGroupEnd());
+  return A2D_OK;
+}
+
+// a2a whose result must end in `dst` (a caller buffer): copy-engine data is
+// moved out of the exchange buffer with one local device copy.
+int a2a_to(Ctx& c, const void* send, void* dst, size_t bytes_per_peer, cudaStream_t s, size_t off) {
+  const void* landed = nullptr;
+  A2D_TRY(a2a(c, send, dst, bytes_per_peer, s, off, &landed));
+  if (landed != dst)
+    CUDA_TRY(cudaMemcpyAsync(dst, landed, bytes_per_peer * c.d_hp, cudaMemcpyDeviceToDevice, s));
   return A2D_OK;
 }
 
@@ -177,6 +228,10 @@ void abort_comms(Ctx& c) {
 int destroy(Ctx* c) {
   if (!c) return A2D_OK;
   cudaDeviceSynchronize();
+  for (int p = 0; p < (int)c->xpeer.size(); ++p)
+    if (c->xpeer[p] && c->xpeer[p] != c->xbuf) cudaIpcCloseMemHandle(c->xpeer[p]);
+  for (cudaStream_t x : c->xs) cudaStreamDestroy(x);
+  for (cudaEvent_t x : c->xe) cudaEventDestroy(x);
   for (ncclComm_t* m : {&c->c_dkv, &c->c_outer, &c->c_inner, &c->hp_comm, &c->world_comm})
     if (*m) ncclCommDestroy(*m);
   for (cudaStream_t s : {c->s_inner, c->s_outer, c->s_dkv})
@@ -190,20 +245,20 @@ int destroy(Ctx* c) {
 
 // dst = this rank's SeqSharded tensor; src HeadSharded (B heads, C tokens, 128):
 // pack [peer][B][L][128] then all-to-all (d_hp = 1: plain copy / conversion)
-int gather_bf16(Ctx& c, const uint16_t* src, int B, uint16_t* dst, cudaStream_t s) {
+int gather_bf16(Ctx& c, const uint16_t* src, int B, uint16_t* dst, cudaStream_t s, size_t off) {
   const size_t chunk = (size_t)B * c.L * 128 * 2;
   if (c.d_hp == 1) {
     CUDA_TRY(cudaMemcpyAsync(dst, src, chunk, cudaMemcpyDeviceToDevice, s));
     return A2D_OK;
   }
   A2D_TRY(a2d_permute_blocks(src, c.g_send, B, c.d_hp, (int64_t)c.L * 128 * 2, s));
-  return a2a(c, c.g_send, dst, chunk, s);
+  return a2a_to(c, c.g_send, dst, chunk, s, off);
 }
 
-int gather_f32_to_bf16(Ctx& c, const float* src, int B, uint16_t* dst, cudaStream_t s) {
+int gather_f32_to_bf16(Ctx& c, const float* src, int B, uint16_t* dst, cudaStream_t s, size_t off) {
   if (c.d_hp == 1) return a2d_permute_f32_to_bf16(src, dst, 1, 1, (int64_t)B * c.C * 128, s);
   A2D_TRY(a2d_permute_f32_to_bf16(src, c.g_send, B, c.d_hp, (int64_t)c.L * 128, s));
-  return a2a(c, c.g_send, dst, (size_t)B * c.L * 128 * 2, s);
+  return a2a_to(c, c.g_send, dst, (size_t)B * c.L * 128 * 2, s, off);
 }
 
 int ring_forward(Ctx& c, const Saved& sv, cudaStream_t s) {
@@ -307,6 +362,77 @@ int ring_backward(Ctx& c, const Saved& sv, const uint16_t* dO, cudaStream_t s, c
   return A2D_OK;
 }
 
+// Copy-engine exchange setup (collective over the HP group): allocate the
+// IN/OUT exchange buffer, share CUDA IPC handles with an NCCL all-gather, map
+// the peers' buffers. Every rank must succeed (all-reduce MIN of a flag) or
+// all fall back to NCCL together. A2D_TRANSPORT=nccl skips it.
+int setup_symm(Ctx& c) {
+  const char* tr = getenv("A2D_TRANSPORT");
+  if (tr && std::string(tr) == "nccl") return A2D_OK;
+  const size_t L128 = (size_t)c.L * 128;
+  c.x_in = (size_t)c.d_hp * L128 * 2 * (c.Hl + 2 * c.Hkl);
+  c.x_out = (size_t)c.d_hp * L128 * (2 * c.Hl + 2 * c.Hkl * (c.rep == 1 ? 2 : 4));
+  c.x_in = (c.x_in + 255) / 256 * 256;
+  int ok = 1;
+  if (cudaMalloc(&c.xbuf, c.x_in + c.x_out) != cudaSuccess) {
+    ok = 0;
+    c.xbuf = nullptr;
+    cudaGetLastError();
+  }
+  cudaIpcMemHandle_t h{};
+  if (ok && cudaIpcGetMemHandle(&h, c.xbuf) != cudaSuccess) {
+    ok = 0;
+    cudaGetLastError();
+  }
+  char* dh = nullptr;
+  CUDA_TRY(cudaMalloc(&dh, (c.d_hp + 1) * sizeof(h)));
+  CUDA_TRY(cudaMemcpy(dh + c.d_hp * sizeof(h), &h, sizeof(h), cudaMemcpyHostToDevice));
+  NCCL_TRY(ncclAllGather(dh + c.d_hp * sizeof(h), dh, sizeof(h), ncclUint8, c.hp_comm, nullptr));
+  CUDA_TRY(cudaDeviceSynchronize());
+  std::vector<cudaIpcMemHandle_t> hs(c.d_hp);
+  CUDA_TRY(cudaMemcpy(hs.data(), dh, c.d_hp * sizeof(h), cudaMemcpyDeviceToHost));
+  c.xpeer.assign(c.d_hp, nullptr);
+  for (int p = 0; p < c.d_hp && ok; ++p) {
+    if (p == c.hp) {
+      c.xpeer[p] = c.xbuf;
+      continue;
+    }
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      ok = 0;
+      cudaGetLastError();
+    } else {
+      c.xpeer[p] = static_cast<char*>(ptr);
+    }
+  }
+  int* dflag = reinterpret_cast<int*>(dh);
+  CUDA_TRY(cudaMemcpy(dflag, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  NCCL_TRY(ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c.hp_comm, nullptr));
+  CUDA_TRY(cudaDeviceSynchronize());
+  int all = 0;
+  CUDA_TRY(cudaMemcpy(&all, dflag, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaFree(dh));
+  if (!all) {  // someone failed: everyone stays on NCCL
+    for (int p = 0; p < c.d_hp; ++p)
+      if (c.xpeer[p] && c.xpeer[p] != c.xbuf) cudaIpcCloseMemHandle(c.xpeer[p]);
+    c.xpeer.clear();
+    if (c.xbuf) cudaFree(c.xbuf);
+    c.xbuf = nullptr;
+    return A2D_OK;
+  }
+  c.allocs.push_back(c.xbuf);
+  A2D_TRY(dalloc(c, &c.xflag, 1));
+  CUDA_TRY(cudaMemset(c.xflag, 0, sizeof(int)));
+  c.xs.resize(c.d_hp - 1);
+  c.xe.resize(c.d_hp - 1);
+  for (int i = 0; i < c.d_hp - 1; ++i) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c.xs[i], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c.xe[i], cudaEventDisableTiming));
+  }
+  c.symm = true;
+  return A2D_OK;
+}
+
 int create(const void* id, int rank, int world, int d_hp, int d_cp, int w, int placement, int H, int Hkv, int d,
            int64_t S, int causal, Ctx** out) {
   if (d != 128) return set_error(A2D_EINVAL, "a2d_ctx_create: the native runtime supports head dim 128");
@@ -407,6 +533,7 @@ int create(const void* id, int rank, int world, int d_hp, int d_cp, int w, int p
     A2D_TRY(dalloc(*c, &c->g32_recv, ge));
     A2D_TRY(dalloc(*c, &c->g32_sum, (size_t)Hkv * c->L * 128));
   }
+  if (d_hp > 1) A2D_TRY(setup_symm(*c));
   CUDA_TRY(cudaDeviceSynchronize());
   return A2D_OK;
 }
@@ -423,13 +550,15 @@ int forward(Ctx& c, const void* q, const void* k, const void* v, void* out, void
     // the state owns its Q (no aliasing of the caller's buffer)
     CUDA_TRY(cudaMemcpyAsync(sv.qh, q, (size_t)c.Hl * L128 * 2, cudaMemcpyDeviceToDevice, s));
   } else {
-    A2D_TRY(a2a(c, q, c.q_recv, (size_t)c.Hl * L128 * 2, s));
-    A2D_TRY(a2a(c, c.kv_send, c.kv_recv, (size_t)2 * c.Hkl * L128 * 2, s));
-    A2D_TRY(a2d_permute_blocks(c.q_recv, sv.qh, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
-    A2D_TRY(a2d_permute_blocks(c.kv_recv, sv.kvh, c.d_hp, 2 * c.Hkl, (int64_t)L128 * 2, s));
+    const size_t qb = (size_t)c.Hl * L128 * 2;
+    const void *q_in = nullptr, *kv_in = nullptr;
+    A2D_TRY(a2a(c, q, c.q_recv, qb, s, 0, &q_in));
+    A2D_TRY(a2a(c, c.kv_send, c.kv_recv, (size_t)2 * c.Hkl * L128 * 2, s, qb * c.d_hp, &kv_in));
+    A2D_TRY(a2d_permute_blocks(q_in, sv.qh, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
+    A2D_TRY(a2d_permute_blocks(kv_in, sv.kvh, c.d_hp, 2 * c.Hkl, (int64_t)L128 * 2, s));
   }
   A2D_TRY(ring_forward(c, sv, s));
-  return gather_bf16(c, sv.out_h, c.Hl, static_cast<uint16_t*>(out), s);
+  return gather_bf16(c, sv.out_h, c.Hl, static_cast<uint16_t*>(out), s, c.x_in);
 }
 
 int backward(Ctx& c, const void* saved, const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
@@ -437,8 +566,9 @@ int backward(Ctx& c, const void* saved, const void* dout, void* dq, void* dk, vo
   const Saved sv = saved_view(c, saved);
   const uint16_t* dO = static_cast<const uint16_t*>(dout);
   if (c.d_hp > 1) {
-    A2D_TRY(a2a(c, dout, c.q_recv, (size_t)c.Hl * L128 * 2, s));
-    A2D_TRY(a2d_permute_blocks(c.q_recv, c.doh, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
+    const void* d_in = nullptr;
+    A2D_TRY(a2a(c, dout, c.q_recv, (size_t)c.Hl * L128 * 2, s, 0, &d_in));
+    A2D_TRY(a2d_permute_blocks(d_in, c.doh, c.d_hp, c.Hl, (int64_t)L128 * 2, s));
     dO = c.doh;
   }
   A2D_TRY(a2d_bwd_preprocess(sv.out_h, dO, sv.lse, c.Hl, c.C, 128, c.lse2, c.delta, s));
@@ -451,22 +581,29 @@ int backward(Ctx& c, const void* saved, const void* dout, void* dq, void* dk, vo
     A2D_TRY(a2d_dqt_to_bf16(c.dq_acc, dq, c.Hl, c.C, c.C_pad, 1, s));
   } else {
     A2D_TRY(a2d_dqt_to_bf16(c.dq_acc, c.g_send, c.Hl, c.C, c.C_pad, c.d_hp, s));
-    A2D_TRY(a2a(c, c.g_send, dq, (size_t)c.Hl * L128 * 2, s));
+    A2D_TRY(a2a_to(c, c.g_send, dq, (size_t)c.Hl * L128 * 2, s, c.x_in));
   }
   const size_t half = (size_t)c.Hkl * c.C * 128;
   void* outs[2] = {dk, dv};
+  // OUT-region offsets: dq at 0, then dk, dv (bf16 chunks, or fp32 for GQA replicas)
+  const size_t q_out = (size_t)c.d_hp * c.Hl * L128 * 2;
+  const size_t k_out = (size_t)c.d_hp * c.Hkl * L128 * (c.rep == 1 ? 2 : 4);
   for (int t = 0; t < 2; ++t) {
+    const size_t off = c.x_in + q_out + t * k_out;
     if (c.rep == 1) {
       if (home_bf16) {
-        A2D_TRY(gather_bf16(c, static_cast<const uint16_t*>(home) + t * half, c.Hkl, static_cast<uint16_t*>(outs[t]), s));
+        A2D_TRY(gather_bf16(c, static_cast<const uint16_t*>(home) + t * half, c.Hkl, static_cast<uint16_t*>(outs[t]), s,
+                            off));
       } else {
-        A2D_TRY(gather_f32_to_bf16(c, static_cast<const float*>(home) + t * half, c.Hkl, static_cast<uint16_t*>(outs[t]), s));
+        A2D_TRY(gather_f32_to_bf16(c, static_cast<const float*>(home) + t * half, c.Hkl,
+                                   static_cast<uint16_t*>(outs[t]), s, off));
       }
     } else {  // GQA replicas: gather fp32, sum the copies, round once
       const float* src = static_cast<const float*>(home) + t * half;
+      const void* g_in = nullptr;
       A2D_TRY(a2d_permute_blocks(src, c.g32_send, c.Hkl, c.d_hp, (int64_t)L128 * 4, s));
-      A2D_TRY(a2a(c, c.g32_send, c.g32_recv, (size_t)c.Hkl * L128 * 4, s));
-      A2D_TRY(a2d_sum_replicas_f32(c.g32_recv, c.g32_sum, c.Hkv, c.rep, (int64_t)L128, s));
+      A2D_TRY(a2a(c, c.g32_send, c.g32_recv, (size_t)c.Hkl * L128 * 4, s, off, &g_in));
+      A2D_TRY(a2d_sum_replicas_f32(static_cast<const float*>(g_in), c.g32_sum, c.Hkv, c.rep, (int64_t)L128, s));
       A2D_TRY(a2d_f32_to_bf16(c.g32_sum, outs[t], (int64_t)c.Hkv * L128, s));
     }
   }
@@ -549,6 +686,12 @@ int a2d_bwd(void* ctx, const void* saved, const void* dout, void* dq, void* dk, 
   Ctx& c = *static_cast<Ctx*>(ctx);
   if (!c.world_comm) return set_error(A2D_EINVAL, "a2d_bwd: context was aborted");
   return backward(c, saved, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+}
+
+int a2d_ctx_transport(void* ctx, int32_t* symm) {
+  if (!ctx || !symm) return set_error(A2D_EINVAL, "a2d_ctx_transport: null argument");
+  *symm = static_cast<Ctx*>(ctx)->symm ? 1 : 0;
+  return A2D_OK;
 }
 
 int a2d_ctx_set_comm(void* ctx, int32_t enabled) {

@@ -43,6 +43,9 @@ class NativeAttn2D:
         _lib.call("a2d_saved_bytes", self._ctx, ctypes.addressof(nb))
         self.saved_bytes = int(nb.value)
         self.saved = None  # state of the last forward() (forward_with_state returns its own)
+        tr = ctypes.c_int32()
+        _lib.call("a2d_ctx_transport", self._ctx, ctypes.addressof(tr))
+        self.transport = "symm" if tr.value else "nccl"
 
     def _empty(self, heads: int, like: torch.Tensor) -> torch.Tensor:
         return torch.empty((heads, self.L, self.model.head_dim), dtype=torch.bfloat16, device=like.device)

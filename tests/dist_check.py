@@ -146,6 +146,7 @@ def main():
             out = nat.forward(*args)
             dq, dk, dv = nat.backward(shard_global(dot, op))
         nat.sync(300.0)
+        nat_transport = nat.transport
         ref_out = op.forward(*args)
         ref_grads = op.backward(shard_global(dot, op))
         torch.cuda.synchronize()
@@ -191,6 +192,7 @@ def main():
         res["head_groups"] = op.ng
         if a.native:
             res["native_vs_python"] = vs_py
+            res["native_transport"] = nat_transport
         print(json.dumps(res))
         if a.out:
             with open(a.out, "w") as f:

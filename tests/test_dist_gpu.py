@@ -186,22 +186,28 @@ NATIVE = [
 ]
 
 
+@pytest.mark.parametrize("transport", ["nccl", "symm"])
 @pytest.mark.parametrize("case", NATIVE, ids=lambda c: "x".join(map(str, c[:3])) + f"-{c[3]}-H{c[4]}-{c[5]}")
-def test_native_runtime_matches_oracle_and_python(case, tmp_path):
+def test_native_runtime_matches_oracle_and_python(case, transport, tmp_path):
     """Native C++ runtime behind the context C ABI: same parity bar
-    as the Python runtime, and the same numbers as dist.Attn2D (NCCL transport)."""
+    as the Python runtime, and the same numbers as dist.Attn2D. transport
+    "symm": the head-parallel exchange on copy engines into CUDA-IPC-mapped
+    peer buffers (d_hp > 1); "nccl": NCCL send/recv."""
     d_hp, d_cp, w, pl, H, Hkv, S = case
     n = d_hp * d_cp
+    if transport == "symm" and d_hp == 1:
+        pytest.skip("no head-parallel exchange at d_hp = 1")
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     res = _run(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
                    "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", "128", "--native"],
-               tmp_path, env={"A2D_TRANSPORT": "nccl"}, timeout=180)
+               tmp_path, env={"A2D_TRANSPORT": transport}, timeout=180)
     for name in ("O", "dQ", "dK", "dV"):
         ma, rl, rng = res[name]
         assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
             f"{name}: max-abs {ma:.3e} (range {rng:.2f}) rel-L2 {rl:.3e}"
     assert res["native_vs_python"] <= 1e-2, res["native_vs_python"]
+    assert res["native_transport"] == transport, res["native_transport"]
 
 
 @pytest.mark.parametrize("case", [(1, 1, 1, "head_first", 4, 2, 1024), (2, 2, 2, "context_first", 8, 4, 2048)],
@@ -216,7 +222,7 @@ def test_native_two_layers_in_flight(case, tmp_path):
         pytest.skip(f"needs {n} GPUs")
     res = _run(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
                    "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", "128", "--native",
-                   "--two-layers"], tmp_path, env={"A2D_TRANSPORT": "nccl"}, timeout=180)
+                   "--two-layers"], tmp_path, timeout=180)
     for name in ("O", "dQ", "dK", "dV"):
         ma, rl, rng = res[name]
         assert ma <= MAX_ABS * max(1.0, rng) and rl <= REL_L2, \
