@@ -205,7 +205,7 @@ def run_reference(a, rank: int, world: int):
     return 0
 
 
-HBM_KERNELS = ("a2d_bwd_preprocess", "a2d_dqt_to_bf16", "a2d_permute_blocks", "a2d_gather_blocks",
+HBM_KERNELS = ("a2d_bwd_preprocess", "a2d_dqt_to_bf16", "a2d_dqt_to_bf16_d", "a2d_permute_blocks", "a2d_gather_blocks",
                "a2d_permute_f32_to_bf16", "a2d_copy_rows", "a2d_merge", "a2d_add_f32", "a2d_f32_to_bf16",
                "a2d_sum_replicas_f32")
 
@@ -252,7 +252,7 @@ def hbm_isolated(H: int, C: int, d: int, dev, peak_gbs: float, reps: int = 5) ->
     a_hp = 4 if H % 4 == 0 else 1
     cases = {
         "a2d_bwd_preprocess": (lambda: K.bwd_preprocess(o, do, lse), H * C * (4 * d + 4) + H * ((C + 63) // 64 * 64) * 8),
-        "a2d_dqt_to_bf16": (lambda: K.dqt_to_bf16(acc, C), H * C * d * 6),
+        "a2d_dqt_to_bf16_d": (lambda: K.dqt_to_bf16(acc, C), H * C * d * 6),
         "a2d_gather_blocks": (lambda: K.gather_blocks(o, idx, dst), 2 * o.numel() * 2),
         "a2d_permute_blocks": (lambda: K.permute_blocks(o, a_hp, H // a_hp, out=dst), 2 * o.numel() * 2),
         "a2d_permute_f32_to_bf16": (lambda: K.permute_to_bf16(f32a, a_hp, H // a_hp, out=dst), 6 * f32a.numel()),
