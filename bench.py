@@ -404,6 +404,8 @@ def main():
     _lib.LOG.reset(timed=("a2d_fa_bwd_chunk", "a2d_fa_fwd_chunk") + HBM_KERNELS)
     _lib.LOG.enabled = True
     n_launch0 = _lib.launch_count()
+    if a.runtime == "native":
+        run.kernel_timing(True)
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -422,6 +424,10 @@ def main():
         if name in kern:
             kern[name][0] += s0.elapsed_time(s1)
             kern[name][1] += 1
+    if a.runtime == "native":  # the C++ runtime brackets its own kernel launches
+        km = run.kernel_ms()
+        run.kernel_timing(False)
+        kern = {"a2d_fa_bwd_chunk": [km["bwd_ms"], km["n_bwd"]], "a2d_fa_fwd_chunk": [km["fwd_ms"], km["n_fwd"]]}
     hbm = hbm_roofline(_lib.LOG.events, peaks()["hbm_gbs"])
     tt = torch.tensor([t_ms, kern["a2d_fa_bwd_chunk"][0], kern["a2d_fa_fwd_chunk"][0]], device=dev,
                       dtype=torch.float64)

@@ -186,6 +186,12 @@ int a2d_ctx_set_comm(void* ctx, int32_t enabled);
  * every HP peer could map the others), 0 = NCCL send/recv (A2D_TRANSPORT=nccl,
  * or any rank failed to map). Ring hops always use NCCL. */
 int a2d_ctx_transport(void* ctx, int32_t* symm);
+/* Measurement: enabled = 1 brackets every attention-kernel launch of the
+ * context with CUDA events on its stream (and resets the record);
+ * a2d_ctx_kernel_ms synchronises and returns the summed forward / backward
+ * kernel milliseconds and launch counts since then. */
+int a2d_ctx_timing(void* ctx, int32_t enabled);
+int a2d_ctx_kernel_ms(void* ctx, float* fwd_ms, float* bwd_ms, int64_t* n_fwd, int64_t* n_bwd);
 int a2d_ctx_destroy(void* ctx);
 /* Host-side plan of the native runtime, exposed for tests and other hosts:
  * CP rank j's ring schedule as (source, outer step, inner step) triples

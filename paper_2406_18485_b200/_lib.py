@@ -45,6 +45,8 @@ SIGNATURES = {
     "a2d_sync": [_vp, _vp, _c_i64],
     "a2d_ctx_set_comm": [_vp, _c_i32],
     "a2d_ctx_transport": [_vp, _vp],
+    "a2d_ctx_timing": [_vp, _c_i32],
+    "a2d_ctx_kernel_ms": [_vp, _vp, _vp, _vp, _vp],
     "a2d_ctx_destroy": [_vp],
     "a2d_ring_plan": [_c_i32, _c_i32, _c_i32, _vp, _vp],
     "a2d_zigzag_positions": [_c_i64, _c_i32, _c_i32, _vp],

@@ -81,7 +81,13 @@ struct Ctx {
   std::vector<cudaStream_t> xs;
   std::vector<cudaEvent_t> xe;
   int* xflag = nullptr;
+  // optional per-kernel CUDA-event timing of the attention kernels (bench roofline)
+  bool timing = false;
+  std::vector<cudaEvent_t> tev[2];  // [0] forward, [1] backward: start/end pairs
+  size_t tused[2] = {0, 0};
 };
+
+
 
 // One forward's state inside the caller's saved buffer (256-byte aligned
 // regions): HeadSharded Q [Hl][C][128] bf16, K/V chunk [2][Hkl][C][128] bf16,
@@ -114,6 +120,19 @@ Saved saved_view(const Ctx& c, const void* base) {
     int rc_ = (x);      \
     if (rc_) return rc_; \
   } while (0)
+
+// Bracket one attention-kernel launch with events on `s` when timing is on.
+int tmark(Ctx& c, int which, cudaStream_t s) {
+  if (!c.timing) return A2D_OK;
+  std::vector<cudaEvent_t>& v = c.tev[which];
+  if (c.tused[which] == v.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    v.push_back(e);
+  }
+  CUDA_TRY(cudaEventRecord(v[c.tused[which]++], s));
+  return A2D_OK;
+}
 
 template <class T>
 int dalloc(Ctx& c, T** p, size_t n) {
@@ -231,6 +250,8 @@ int destroy(Ctx* c) {
   for (int p = 0; p < (int)c->xpeer.size(); ++p)
     if (c->xpeer[p] && c->xpeer[p] != c->xbuf) cudaIpcCloseMemHandle(c->xpeer[p]);
   for (cudaStream_t x : c->xs) cudaStreamDestroy(x);
+  for (auto& v : c->tev)
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
   for (cudaEvent_t x : c->xe) cudaEventDestroy(x);
   for (ncclComm_t* m : {&c->c_dkv, &c->c_outer, &c->c_inner, &c->hp_comm, &c->world_comm})
     if (*m) ncclCommDestroy(*m);
@@ -264,9 +285,12 @@ int gather_f32_to_bf16(Ctx& c, const float* src, int B, uint16_t* dst, cudaStrea
 int ring_forward(Ctx& c, const Saved& sv, cudaStream_t s) {
   const size_t kv_elems = (size_t)2 * c.Hkl * c.C * 128, kv_bytes = kv_elems * 2, half = kv_elems / 2;
   const int64_t q_rows = (int64_t)c.C;
-  if (c.d_cp == 1)
-    return a2d_fa_fwd_chunk(sv.qh, sv.kvh, sv.kvh + half, c.pos[c.cp], c.pos[c.cp], c.b128[c.cp], c.b128[c.cp], c.Hl,
-                            c.Hkl, q_rows, q_rows, 128, c.causal, c.scale, 0, sv.lse, nullptr, sv.out_h, s);
+  if (c.d_cp == 1) {
+    A2D_TRY(tmark(c, 0, s));
+    A2D_TRY(a2d_fa_fwd_chunk(sv.qh, sv.kvh, sv.kvh + half, c.pos[c.cp], c.pos[c.cp], c.b128[c.cp], c.b128[c.cp], c.Hl,
+                             c.Hkl, q_rows, q_rows, 128, c.causal, c.scale, 0, sv.lse, nullptr, sv.out_h, s));
+    return tmark(c, 0, s);
+  }
   const uint16_t *cur = sv.kvh, *first = sv.kvh;
   uint16_t* nxt_inner = nullptr;
   uint16_t* nxt_outer = nullptr;
@@ -284,9 +308,11 @@ int ring_forward(Ctx& c, const Saved& sv, cudaStream_t s) {
       nxt_inner = c.ring[(t + 1) % 2];
       A2D_TRY(hop(c, c.c_inner, c.s_inner, s, cur, c.inner_to, nxt_inner, c.inner_from, kv_bytes, c.ev_inner));
     }
+    A2D_TRY(tmark(c, 0, s));
     A2D_TRY(a2d_fa_fwd_chunk(sv.qh, cur, cur + half, c.pos[c.cp], c.pos[step.source], c.b128[c.cp],
                              c.b128[step.source], c.Hl, c.Hkl, q_rows, q_rows, 128, c.causal, c.scale, st > 0 ? 1 : 0,
                              sv.lse, c.acc, last ? sv.out_h : nullptr, s));
+    A2D_TRY(tmark(c, 0, s));
     if (t + 1 < c.w) {
       CUDA_TRY(cudaStreamWaitEvent(s, c.ev_inner, 0));
       cur = nxt_inner;
@@ -304,9 +330,11 @@ int ring_backward(Ctx& c, const Saved& sv, const uint16_t* dO, cudaStream_t s, c
   const int64_t T = (int64_t)c.C;
   const uint16_t* kv_own = sv.kvh;
   if (c.d_cp == 1) {
+    A2D_TRY(tmark(c, 1, s));
     A2D_TRY(a2d_fa_bwd_chunk(sv.qh, kv_own, kv_own + half, dO, c.pos[c.cp], c.pos[c.cp], c.b64[c.cp], c.b128[c.cp],
                              c.lse2, c.delta, c.dq_acc, c.dkv, c.dkv + half, 0, c.Hl, c.Hkl, T, T, 128, c.causal,
                              c.scale, s));
+    A2D_TRY(tmark(c, 1, s));
     *home = c.dkv;
     *home_bf16 = false;
     return A2D_OK;
@@ -329,9 +357,11 @@ int ring_backward(Ctx& c, const Saved& sv, const uint16_t* dO, cudaStream_t s, c
       A2D_TRY(hop(c, c.c_inner, c.s_inner, s, cur, c.inner_to, nxt_inner, c.inner_from, kv_bytes, c.ev_inner));
     }
     float* tgt = st == 0 ? c.dacc[0] : c.part;
+    A2D_TRY(tmark(c, 1, s));
     A2D_TRY(a2d_fa_bwd_chunk(sv.qh, cur, cur + half, dO, c.pos[c.cp], c.pos[step.source], c.b64[c.cp],
                              c.b128[step.source], c.lse2, c.delta, c.dq_acc, tgt, tgt + half, 0, c.Hl, c.Hkl, T, T, 128,
                              c.causal, c.scale, s));
+    A2D_TRY(tmark(c, 1, s));
     if (st > 0) {  // the travelling accumulator of this chunk arrived in dacc[st % 2]
       CUDA_TRY(cudaStreamWaitEvent(s, c.ev_dkv, 0));
       A2D_TRY(a2d_add_f32(c.dacc[st % 2], c.part, (int64_t)kv_elems, s));
@@ -686,6 +716,33 @@ int a2d_bwd(void* ctx, const void* saved, const void* dout, void* dq, void* dk, 
   Ctx& c = *static_cast<Ctx*>(ctx);
   if (!c.world_comm) return set_error(A2D_EINVAL, "a2d_bwd: context was aborted");
   return backward(c, saved, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+}
+
+int a2d_ctx_timing(void* ctx, int32_t enabled) {
+  if (!ctx) return set_error(A2D_EINVAL, "a2d_ctx_timing: null context");
+  Ctx& c = *static_cast<Ctx*>(ctx);
+  c.timing = enabled != 0;
+  c.tused[0] = c.tused[1] = 0;
+  return A2D_OK;
+}
+
+int a2d_ctx_kernel_ms(void* ctx, float* fwd_ms, float* bwd_ms, int64_t* n_fwd, int64_t* n_bwd) {
+  if (!ctx || !fwd_ms || !bwd_ms || !n_fwd || !n_bwd) return set_error(A2D_EINVAL, "a2d_ctx_kernel_ms: null argument");
+  Ctx& c = *static_cast<Ctx*>(ctx);
+  CUDA_TRY(cudaDeviceSynchronize());
+  float* outs[2] = {fwd_ms, bwd_ms};
+  int64_t* ns[2] = {n_fwd, n_bwd};
+  for (int w = 0; w < 2; ++w) {
+    float tot = 0.f;
+    for (size_t i = 0; i + 1 < c.tused[w]; i += 2) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, c.tev[w][i], c.tev[w][i + 1]));
+      tot += ms;
+    }
+    *outs[w] = tot;
+    *ns[w] = (int64_t)(c.tused[w] / 2);
+  }
+  return A2D_OK;
 }
 
 int a2d_ctx_transport(void* ctx, int32_t* symm) {

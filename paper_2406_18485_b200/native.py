@@ -90,6 +90,18 @@ class NativeAttn2D:
         self._comm = bool(on)
         _lib.call("a2d_ctx_set_comm", self._ctx, int(self._comm))
 
+    def kernel_timing(self, enabled: bool) -> None:
+        """Start (and reset) / stop CUDA-event timing of the attention kernels."""
+        _lib.call("a2d_ctx_timing", self._ctx, int(enabled))
+
+    def kernel_ms(self) -> dict:
+        """Summed fwd / bwd attention-kernel milliseconds since kernel_timing(True)."""
+        f, b = ctypes.c_float(), ctypes.c_float()
+        nf, nb = ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("a2d_ctx_kernel_ms", self._ctx, ctypes.addressof(f), ctypes.addressof(b), ctypes.addressof(nf),
+                  ctypes.addressof(nb))
+        return {"fwd_ms": f.value, "bwd_ms": b.value, "n_fwd": nf.value, "n_bwd": nb.value}
+
     def sync(self, timeout_s: float = 600.0) -> None:
         """Wait for this rank's queued layer work, polling NCCL for asynchronous
         errors; raises (and aborts the communicators) on an error or timeout."""

@@ -31,7 +31,7 @@ def metrics(got, ref):
             float(np.abs(ref).max()))
 
 
-def sampled_check(a, op, rank, qt, kt, vt, dot, out, dq, dk, dv):
+def sampled_check(a, op, rank, qt, kt, vt, dot, out, dq, dk, dv, lse=None):
     """Gather the SeqSharded outputs (and the HeadSharded LSE of the plain
     path) to global natural order on the GPU; rank 0 checks sampled rows/keys
     of the first and last KV-head groups against the f64 oracle."""
@@ -46,8 +46,10 @@ def sampled_check(a, op, rank, qt, kt, vt, dot, out, dq, dk, dv):
 
     O, DQ, DK, DV = (gather_dev(x) for x in (out, dq, dk, dv))
     LSE = None
-    if op.saved is not None and not a.fused_qkv and not a.native:
-        lse = op.saved[3].contiguous()  # HeadSharded (Hl, C): heads hp*Hl.., positions of CP chunk cp
+    if lse is None and op.saved is not None and not a.fused_qkv and not a.native:
+        lse = op.saved[3]
+    if lse is not None:
+        lse = lse.contiguous()  # HeadSharded (Hl, C): heads hp*Hl.., positions of CP chunk cp
         parts = [torch.empty_like(lse) for _ in range(world)]
         dist.all_gather(parts, lse)
         LSE = torch.empty((a.heads, a.seq), dtype=torch.float32, device=lse.device)
@@ -147,6 +149,7 @@ def main():
             dq, dk, dv = nat.backward(shard_global(dot, op))
         nat.sync(300.0)
         nat_transport = nat.transport
+        nat_lse = nat.lse_of(st_a if a.two_layers else nat.saved).clone()
         ref_out = op.forward(*args)
         ref_grads = op.backward(shard_global(dot, op))
         torch.cuda.synchronize()
@@ -164,7 +167,7 @@ def main():
         return unshard_global(parts, op).float().cpu().numpy()
 
     if a.sampled:
-        res = sampled_check(a, op, rank, qt, kt, vt, dot, out, dq, dk, dv)
+        res = sampled_check(a, op, rank, qt, kt, vt, dot, out, dq, dk, dv, nat_lse if a.native else None)
         if rank == 0:
             print(json.dumps(res))
             if a.out:

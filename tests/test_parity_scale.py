@@ -32,6 +32,7 @@ SCALE_CASES = [
     (1, 1, 1, "head_first", 32, 32, 32768, 128, {}),
     (1, 1, 1, "head_first", 32, 32, 131072, 128, {}),
     (1, 1, 1, "head_first", 32, 8, 65536, 128, {}),
+    (1, 1, 1, "head_first", 8, 8, 32768, 64, {}),  # config 1's head dim (d=64 forward AND backward kernels)
     # 2 GPUs
     (2, 1, 1, "head_first", 32, 32, 32768, 128, {}),
     (1, 2, 2, "context_first", 32, 8, 32768, 128, {}),
@@ -39,6 +40,7 @@ SCALE_CASES = [
     (2, 2, 2, "head_first", 32, 32, 65536, 128, {}),
     (2, 2, 2, "head_first", 32, 32, 65536, 128, {"A2D_TRANSPORT": "nccl"}),
     (2, 2, 1, "context_first", 32, 8, 32768, 128, {}),
+    (2, 2, 2, "head_first", 32, 8, 65536, 128, {"native": 1}),  # native C++ runtime, copy-engine exchange
     (1, 4, 2, "head_first", 32, 32, 32768, 128, {}),
     (4, 1, 1, "context_first", 32, 2, 16384, 128, {}),  # GQA replication: H_kv=2 < d_hp=4
     # 8 GPUs: config 3 (4x2, both placements, w=1/2), config 4 (GQA 2x4 w=2),
@@ -54,6 +56,7 @@ SCALE_CASES = [
 
 def _ids(c):
     tag = "-nccl" if c[8].get("A2D_TRANSPORT") == "nccl" else ""
+    tag += "-native" if c[8].get("native") else ""
     return f"{c[0]}x{c[1]}w{c[2]}-{c[3]}-H{c[4]}-{c[5]}-S{c[6]}-d{c[7]}{tag}"
 
 
@@ -73,9 +76,11 @@ def test_sampled_parity_at_scale(case, tmp_path):
     n = d_hp * d_cp
     if not torch.cuda.is_available() or torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
+    env = dict(env)
+    native = env.pop("native", None)
     res = run_sampled(n, ["--d-hp", str(d_hp), "--d-cp", str(d_cp), "--w", str(w), "--placement", pl,
-                          "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", str(d)],
-                      env, tmp_path)
+                          "--heads", str(H), "--kv-heads", str(Hkv), "--seq", str(S), "--dim", str(d)]
+                      + (["--native"] if native else []), env, tmp_path)
     print(_ids(case), json.dumps({k: res[k] for k in ("O", "LSE", "dQ", "dK", "dV", "dK_vs_bf16ops", "dV_vs_bf16ops", "pin_lse", "pin_delta", "deviations")
                                   if k in res}))
     assert "LSE" in res and res["rows"] >= 512 and res["keys"] >= 256
