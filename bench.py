@@ -44,8 +44,11 @@ UNIT = "TFLOP/s"
 
 
 def default_grid(n: int):
-    """(d_hp, d_cp, w) per GPU count: BASELINE config 3 is 4x2 at 8 GPUs."""
-    return {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 2), 8: (4, 2, 2)}.get(n, (n, 1, 1))
+    """(d_hp, d_cp, w) per GPU count. N=2, 4: the fastest factorisation of the
+    measured S=128K sweep (profiles/r02_final_sweep_S128k_2_4gpu.jsonl; also the
+    planner's pick, tools/plan.py); N=8: BASELINE config 3's 4x2 grid, inner
+    ring w=1 (w=1 beat w=2 by 1.7% at 2x2 in the same sweep)."""
+    return {1: (1, 1, 1), 2: (2, 1, 1), 4: (4, 1, 1), 8: (4, 2, 1)}.get(n, (n, 1, 1))
 
 
 def peaks():
