@@ -223,6 +223,8 @@ int a2d_fa_bwd_chunk(const void* q, const void* k, const void* v, const void* do
       p.tm_dq = p.tm_k;
       p.tm_dq8 = p.tm_k;
     }
+    p.dq = len > 0 ? dq_acc + off : nullptr;
+    p.dq_ld = tq_pad;
     p.q_pos = q_pos + off;
     p.k_pos = k_pos;
     p.q_bounds = reinterpret_cast<const int2*>(q_bounds64) + off / 64;

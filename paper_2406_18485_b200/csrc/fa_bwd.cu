@@ -190,14 +190,10 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   const int n_live = bars.n_live;
   const int n = n_live * p.G;  // iterations: (g, live tile) g-major
   // register budget: TMA/MMA warpgroup and drain warpgroup give registers to
-  // the two P/dS warpgroups (80*128 + 96*128 + 2*152*128 <= 64K)
-  if (warp < 4) {
-    regs_dec<80>();
-  } else if (warp >= 12) {
-    regs_dec<96>();
-  } else {
-    regs_inc<152>();
-  }
+  // the two P/dS warpgroups (80*128 + 96*128 + 2*152*128 <= 64K); the
+  // drain / P/dS adjustments sit inside their role branches so ptxas
+  // allocates each role at its own budget
+  if (warp < 4) regs_dec<80>();
 
   long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   (void)prof;
@@ -341,6 +337,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     // TMEM lane = feature d; 64 query columns -> two SW128 smem boxes -> TMA
     // bulk reduce-add into the transposed dq_acc. Runs concurrently with the
     // P/dS warpgroups, off their critical path.
+    regs_dec<96>();
     const int wq = warp % 4;
     const int d = wq * 32 + lane;
     const bool d_ok = d < D;  // D = 64: warps 14-15 only keep the barriers
@@ -434,6 +431,7 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
     // ------------------------------------------------ P/dS warpgroups
     // Both warpgroups cover all 128 key rows (TMEM lanes); warpgroup hq owns
     // query columns [32*hq, 32*hq+32) of every iteration.
+    regs_inc<152>();
     const int hq = (warp - 4) / 4;
     const int wq = warp % 4;
     const int r = wq * 32 + lane;
@@ -561,6 +559,8 @@ __global__ void __launch_bounds__(bwd::kThreads, 1) fa_bwd_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+#include "fa_bwd_q128.cuh"
+
 template <int D, int QST, int PF, bool DQ8 = false>
 static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
   constexpr int bytes = bwd::Cfg<D, QST, DQ8>::kBytes;
@@ -573,9 +573,13 @@ static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Experiment switch (A2D_BWD_VARIANT, read once): 0 default (3 stages, no
-// prefetch), 1 = 2 stages, 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead,
-// 4 = 4 stages with the per-warp 8-query dQ drain, 5 = 3 stages with it.
+// Experiment switch (A2D_BWD_VARIANT, read once): 0 default (D = 128: the
+// 128-query kernel, fa_bwd_q128.cuh, 1 dO stage + dedicated drain staging;
+// D = 64: the 64-query kernel), 7 = the 128-query kernel with 2 dO stages
+// and the drain staging in the dS^T buffer, 6 = the
+// 64-query kernel at D = 128 (3 stages, no prefetch), 1 = it with 2 stages,
+// 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead, 4 = 4 stages with the
+// per-warp 8-query dQ drain, 5 = 3 stages with it.
 static int bwd_variant() {
   static int v = -1;
   if (v < 0) {
@@ -596,7 +600,9 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
     case 3: return launch_bwd_d<128, 3, 8>(p, s);
     case 4: return launch_bwd_d<128, 4, 0, true>(p, s);
     case 5: return launch_bwd_d<128, 3, 0, true>(p, s);
-    default: return launch_bwd_d<128, 3, 0>(p, s);
+    case 6: return launch_bwd_d<128, 3, 0>(p, s);
+    case 7: return launch_bwd_q128<128, false>(p, s);
+    default: return launch_bwd_q128<128, true>(p, s);
   }
 }
 

@@ -1,0 +1,526 @@
+// K3, round-3 structure: 128-query iterations, every GEMM at N = 128.
+// (Included by fa_bwd.cu; shares its wait-time instrumentation.)
+//
+// Same math as fa_bwd_kernel (ref oracle.py:127-152): P = exp(S - LSE),
+// dP = dO V^T, dS = P (dP - delta), dV += P^T dO, dK += dS^T Q, dQ += dS K.
+//
+// Why: the 64-query kernel issues three of its five GEMMs (S^T, dP^T, dQ^T)
+// as SS UMMAs with N = 64, which need 192 B/clk of shared-memory operands
+// against the 128 B/clk the SM delivers (tools/probes/umma_rate.cu: 66.7 % of
+// peak). With 128 queries per iteration every SS GEMM has
+// N = 128 (128 B/clk, 100 % in the probe) and the operand bytes per FLOP of
+// S^T/dP^T/dQ^T drop by a third.
+//
+// TMEM (512 columns) holds no double buffers any more; the in-order tensor
+// pipe does the hand-off instead:
+//   R_S  [0,128)    S^T_i (keys x queries)  -> P^T_i  (bf16, TS A of dV)
+//   R_dP [128,256)  dP^T_i                  -> dS^T_i (bf16, TS A of dK)
+//                                           -> dQ^T_i = K^T dS^T_i (M = d)
+//   [256,384) dV,   [384,512) dK accumulators.
+// Issue order per iteration:  dV_i, S_{i+1}, dK_i, dQ^T_i, dP_{i+1}.
+//   S_{i+1} overwrites P^T_i right after dV_i (its only reader) and
+//   dQ^T_i overwrites dS^T_i right after dK_i: tcgen05.mma ops of one thread
+//   execute in issue order (the 64-query kernel relies on the same property
+//   for S^T_{i+2} over P^T_i). S_{i+1} is issued before dK_i/dQ^T_i so the
+//   softmax of i+1 (MUFU-bound, ~1000 clk) runs under three GEMMs; the only
+//   exposed hand-off is the dQ^T drain's TMEM read before dP_{i+1}.
+// Shared memory (D = 128): K 32 KB, V 32 KB, 2 Q/dO stages 128 KB, dS^T
+// 32 KB = 224 KB; the dS^T buffer doubles as the dQ^T drain's staging (it is
+// free between dQ^T_i's completion and the softmax's dS_{i+1} store, which
+// waits for the drain). The live query-tile list is a bitmask (2 x 128 B).
+// Warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4-11 two P/dS
+// warpgroups (warpgroup hq owns queries [64hq, 64hq+64) of every iteration,
+// all 128 keys = TMEM lanes), 12-15 the dQ^T drain (TMEM lane = feature d).
+
+namespace bwd2 {
+constexpr int BK = 128;
+constexpr int BQ = 128;
+constexpr int QST = 2;
+constexpr int kThreads = 512;
+constexpr int kMaxQTiles = 1024;  // per launch (the C ABI slices at 131072 queries)
+constexpr int kWords = kMaxQTiles / 32;
+// DO1: one dO stage instead of two; the 32 KB it frees become the dQ^T
+// drain's own staging (otherwise the drain borrows the dS^T buffer).
+template <int D, bool DO1>
+struct Cfg {
+  static constexpr int kDOST = DO1 ? 1 : 2;              // dO stages (Q always has 2)
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + BK * D * 2;
+  static constexpr int kQ = kV + BK * D * 2;             // QST x [D/64 panels][128 q][64] SW128
+  static constexpr int kDO = kQ + QST * BQ * D * 2;
+  static constexpr int kDS = kDO + kDOST * BQ * D * 2;   // dS^T [2 panels][128 keys][64 q] SW128
+  static constexpr int kSTG = kDS + BK * BQ * 2;         // drain staging: 2 SW128 boxes [D][32 q] fp32 (DO1)
+  static constexpr int kStats = kSTG + (DO1 ? 2 * D * 128 : 0);  // QST x (lse2[128], delta[128])
+  static constexpr int kMask = kStats + QST * 2 * BQ * 4;  // live bits, full bits
+  static constexpr int kBars = kMask + 2 * kWords * 4;
+  static constexpr int kBytes = kBars + 256;
+  static constexpr int kQStage = BQ * D * 2;              // bytes of one Q (or dO) stage
+  static constexpr int kPanels = D / 64;
+};
+struct Bars {
+  uint64_t kv_full;
+  uint64_t q_full[QST], q_empty[QST], do_full[QST], do_empty[QST];
+  uint64_t s_full, dp_full, p_full, dst_full, dss_full, dq_full, dq_empty, dsbuf_free, dkv_full;
+  uint32_t tmem_base;
+};
+static_assert(sizeof(Bars) <= 256, "barrier block");
+
+// Live query tiles, highest first (the order every role walks them in).
+struct LiveIt {
+  const uint32_t* live;
+  int wi;
+  uint32_t m;
+  A2D_DEV void reset(const uint32_t* l, int nwords) {
+    live = l;
+    wi = nwords - 1;
+    m = nwords > 0 ? l[wi] : 0u;
+  }
+  A2D_DEV int next() {
+    while (m == 0u) m = live[--wi];
+    const int b = 31 - __clz(m);
+    m ^= 1u << b;
+    return wi * 32 + b;
+  }
+};
+}  // namespace bwd2
+
+template <int D, bool DO1>
+__global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __grid_constant__ BwdParams p) {
+  using namespace bwd2;
+  using C = Cfg<D, DO1>;
+  constexpr int NDO = C::kDOST;
+  static_assert(D == 128, "the 128-query backward is built for head dim 128");
+  constexpr int kK = C::kK, kV = C::kV, kQ = C::kQ, kDO = C::kDO, kDS = C::kDS, kStats = C::kStats;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  Bars& bars = *reinterpret_cast<Bars*>(smem + C::kBars);
+  uint32_t* live_mask = reinterpret_cast<uint32_t*>(smem + C::kMask);
+  uint32_t* full_mask = live_mask + kWords;
+
+  const int warp = warp_id(), lane = lane_id();
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SW128 operands need a 1 KB aligned base
+  const int kt = (int)blockIdx.x;
+  const int hk = blockIdx.y;
+  const int key0 = kt * BK;
+  const int nqt64 = (p.Tq + 63) / 64;
+  const int nqt = (p.Tq + BQ - 1) / BQ;
+  const int nwords = (nqt + 31) / 32;
+  const int Tq_pad = p.stats_stride;
+  const int2 kb = p.k_bounds[kt];
+  const bool causal = p.causal != 0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.kv_full, 1);
+    for (int i = 0; i < QST; ++i) {
+      mbar_init(&bars.q_full[i], 1); mbar_init(&bars.q_empty[i], 1);
+      mbar_init(&bars.do_full[i], 1); mbar_init(&bars.do_empty[i], 1);
+    }
+    mbar_init(&bars.s_full, 1);
+    mbar_init(&bars.dp_full, 1);
+    mbar_init(&bars.p_full, 256);
+    mbar_init(&bars.dst_full, 256);
+    mbar_init(&bars.dss_full, 256);
+    mbar_init(&bars.dq_full, 1);
+    mbar_init(&bars.dq_empty, 128);
+    mbar_init(&bars.dsbuf_free, 1);
+    mbar_init(&bars.dkv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars.tmem_base);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tm_q); tma_prefetch(&p.tm_k); tma_prefetch(&p.tm_v); tma_prefetch(&p.tm_do);
+    tma_prefetch(&p.tm_dq);
+  }
+  // ---- live / full bitmasks over 128-query tiles (from the 64-row bounds)
+  for (int wi = warp; wi < nwords; wi += 16) {
+    const int t = wi * 32 + lane;
+    bool lv = false, full = false;
+    if (t < nqt) {
+      int2 qb = p.q_bounds[2 * t];
+      const bool two = 2 * t + 1 < nqt64;
+      if (two) {
+        const int2 b1 = p.q_bounds[2 * t + 1];
+        qb = make_int2(min(qb.x, b1.x), max(qb.y, b1.y));
+      }
+      lv = qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y);
+      // full: no mask needed. A tile reaching past the 64-padded stats
+      // (single 64-row half) is always masked.
+      full = two && (!causal || kb.y <= qb.x);
+    }
+    const unsigned lm = __ballot_sync(0xffffffffu, lv), fm = __ballot_sync(0xffffffffu, full);
+    if (lane == 0) { live_mask[wi] = lm; full_mask[wi] = fm; }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+  int n_live = 0;
+  for (int wi = 0; wi < nwords; ++wi) n_live += __popc(live_mask[wi]);
+  const int n = n_live * p.G;  // iterations: (g, live tile), g-major
+  // register budget (setmaxnreg inside each role's branch, so ptxas allocates
+  // each role at its own budget): 64 (TMA/MMA/alloc) + 2 x 144 (P/dS) + 160
+  // (drain) = 512 per lane x 128
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  (void)prof;
+  if (warp < 4) regs_dec<64>();
+  if (warp == 0) {
+    // -------------------------------------------------------------- producer
+    PSTART();
+    if (lane == 0 && n > 0) {
+      mbar_expect_tx(&bars.kv_full, 2 * BK * D * 2);
+      for (int c = 0; c < C::kPanels; ++c) {
+        tma_load_3d(smem + kK + c * 16384, &p.tm_k, &bars.kv_full, c * 64, key0, hk);
+        tma_load_3d(smem + kV + c * 16384, &p.tm_v, &bars.kv_full, c * 64, key0, hk);
+      }
+      LiveIt li;
+      int it = 0;
+      for (int g = 0; g < p.G; ++g) {
+        const int h = hk * p.G + g;
+        li.reset(live_mask, nwords);
+        for (int j = 0; j < n_live; ++j, ++it) {
+          const int qt = li.next();
+          const int qs = it % QST, ds = it % NDO;
+          // Q (+ the stats) once dK_{it-2} freed the stage, dO once dV_{it-NDO} did
+          PWAIT(&bars.q_empty[qs], ((it / QST) & 1) ^ 1, 0);
+          // stats: 128 rows, or 64 when the tile's second half lies past the
+          // 64-row padding of the stats (then the tile is on the masked path)
+          const int nst = (2 * qt + 1 < nqt64) ? BQ : 64;
+          mbar_expect_tx(&bars.q_full[qs], C::kQStage + 2 * nst * 4);
+          uint8_t* sq = smem + kQ + qs * C::kQStage;
+          for (int c = 0; c < C::kPanels; ++c)
+            for (int hh = 0; hh < 2; ++hh)
+              tma_load_3d(sq + c * 16384 + hh * 8192, &p.tm_q, &bars.q_full[qs], c * 64, qt * BQ + hh * 64, h);
+          float* st = reinterpret_cast<float*>(smem + kStats) + qs * 2 * BQ;
+          bulk_g2s(st, p.lse2 + (size_t)h * Tq_pad + qt * BQ, nst * 4, &bars.q_full[qs]);
+          bulk_g2s(st + BQ, p.delta + (size_t)h * Tq_pad + qt * BQ, nst * 4, &bars.q_full[qs]);
+          PWAIT(&bars.do_empty[ds], ((it / NDO) & 1) ^ 1, 1);
+          mbar_expect_tx(&bars.do_full[ds], C::kQStage);
+          uint8_t* sd = smem + kDO + ds * C::kQStage;
+          for (int c = 0; c < C::kPanels; ++c)
+            for (int hh = 0; hh < 2; ++hh)
+              tma_load_3d(sd + c * 16384 + hh * 8192, &p.tm_do, &bars.do_full[ds], c * 64, qt * BQ + hh * 64, h);
+        }
+      }
+    }
+    PFLUSH(3);
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- MMA issuer
+    PSTART();
+    if (n > 0) {
+      constexpr uint32_t id_s = idesc_bf16(BK, BQ, false, false);  // S^T, dP^T: M=128 keys, N=128 q
+      constexpr uint32_t id_kv = idesc_bf16(BK, D, false, true);   // dV, dK: TS, B MN-major
+      constexpr uint32_t id_dq = idesc_bf16(D, BQ, true, true);    // dQ^T: M=d, N=128 q
+      const uint32_t sK = smem_u32(smem + kK), sV = smem_u32(smem + kV);
+      const uint32_t sQ = smem_u32(smem + kQ), sDO = smem_u32(smem + kDO);
+      const uint32_t sDS = smem_u32(smem + kDS);
+      const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+      const uint64_t dK0 = sdesc_sw128(sK, 16, 1024), dV0 = sdesc_sw128(sV, 16, 1024);
+      const uint64_t dQ0 = sdesc_sw128(sQ, 16, 1024), dDO0 = sdesc_sw128(sDO, 16, 1024);
+      const uint64_t dKmn = sdesc_sw128(sK, 16384, 1024);   // K as MN-major A (M = d) of dQ^T
+      const uint64_t dDSmn = sdesc_sw128(sDS, 16384, 1024); // dS^T as MN-major B (N = q) of dQ^T
+      const uint64_t dQmn = sdesc_sw128(sQ, 16384, 1024), dDOmn = sdesc_sw128(sDO, 16384, 1024);
+      constexpr uint64_t kStage = (uint64_t)(C::kQStage >> 4);
+      // S^T_i (which = 0) or dP^T_i (which = 1): M=128 keys, N=128 q, K=d
+      auto issue_sdp = [&](int i, int which) {
+        const uint64_t qoff = (uint64_t)(which == 0 ? i % QST : i % NDO) * kStage;
+        __syncwarp();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t ka = (uint64_t)(((k / 4) * 16384 + (k % 4) * 32) >> 4);
+            if (which == 0)
+              umma_ss(tS, dK0 + ka, dQ0 + qoff + ka, id_s, k > 0);
+            else
+              umma_ss(tDP, dV0 + ka, dDO0 + qoff + ka, id_s, k > 0);
+          }
+          umma_commit(which == 0 ? &bars.s_full : &bars.dp_full);
+        }
+        __syncwarp();
+      };
+      PWAIT(&bars.kv_full, 0, 0);
+      PWAIT(&bars.q_full[0], 0, 1);
+      tc_fence_after();
+      issue_sdp(0, 0);
+      PWAIT(&bars.do_full[0], 0, 6);
+      tc_fence_after();
+      issue_sdp(0, 1);
+      for (int i = 0; i < n; ++i) {
+        const int qs = i % QST, ds = i % NDO;
+        const uint32_t ph = i & 1;
+        const uint64_t qoff = (uint64_t)qs * kStage, doff = (uint64_t)ds * kStage;
+        // dV += P^T_i dO_i (TS: P^T in R_S; 16 queries per K step at col 32(k/2)+8(k%2))
+        PWAIT(&bars.p_full, ph, 2);
+        tc_fence_after();
+        __syncwarp();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BQ / 16; ++k)
+            umma_ts(tDV, tS + (k / 2) * 32 + (k % 2) * 8, dDOmn + doff + (uint64_t)(k * 128), id_kv,
+                    (i > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&bars.do_empty[ds]);  // dO_i's last reader
+        }
+        __syncwarp();
+        // S^T_{i+1} into R_S (after dV_i in the in-order pipe)
+        if (i + 1 < n) {
+          PWAIT(&bars.q_full[(i + 1) % QST], ((i + 1) / QST) & 1, 1);
+          tc_fence_after();
+          issue_sdp(i + 1, 0);
+        }
+        // dK += dS^T_i Q_i (TS: dS^T in R_dP), then release Q_i/dO_i
+        PWAIT(&bars.dst_full, ph, 4);
+        tc_fence_after();
+        __syncwarp();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BQ / 16; ++k)
+            umma_ts(tDK, tDP + (k / 2) * 32 + (k % 2) * 8, dQmn + qoff + (uint64_t)(k * 128), id_kv,
+                    (i > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&bars.q_empty[qs]);
+        }
+        __syncwarp();
+        // dQ^T_i = K^T dS^T_i into R_dP (after dK_i); dS^T from shared memory
+        PWAIT(&bars.dss_full, ph, 5);
+        tc_fence_after();
+        __syncwarp();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_ss(tDP, dKmn + (uint64_t)(k * 128), dDSmn + (uint64_t)(k * 128), id_dq, k > 0);
+          umma_commit(&bars.dq_full);
+        }
+        __syncwarp();
+        // dP^T_{i+1} into R_dP once the drain has read dQ^T_i
+        if (i + 1 < n) {
+          PWAIT(&bars.dq_empty, ph, 3);
+          PWAIT(&bars.do_full[(i + 1) % NDO], ((i + 1) / NDO) & 1, 6);
+          tc_fence_after();
+          issue_sdp(i + 1, 1);
+        }
+      }
+      __syncwarp();
+      if (elect_one()) umma_commit(&bars.dkv_full);
+      __syncwarp();
+    }
+    PFLUSH(0);
+  } else if (warp >= 12) {
+    // ------------------------------------------------ dQ^T drain warpgroup
+    // Reads all of R_dP (TMEM lane = feature d, column = query) and releases
+    // it for dP_{i+1}; then streams the 128 queries as four SW128 boxes
+    // [128 d][32 q] through the two halves of the dS^T buffer (free from
+    // dQ^T_i's completion until the softmax stores dS_{i+1}) into TMA bulk
+    // reduce-adds on the transposed fp32 dq_acc, two boxes in flight.
+    // (red.global from registers measured 2x slower: 1-sector L2 requests.)
+    regs_inc<160>();
+    const int wq = warp % 4;
+    const int d = wq * 32 + lane;
+    PSTART();
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    uint8_t* stage = smem + (DO1 ? C::kSTG : kDS);
+    const bool leader = warp == 12 && lane == 0;
+    const float scale = p.scale;
+    LiveIt li;
+    int it = 0;
+    for (int g = 0; g < p.G; ++g) {
+      const int h = hk * p.G + g;
+      li.reset(live_mask, nwords);
+      for (int j = 0; j < n_live; ++j, ++it) {
+        const int qt = li.next();
+        PWAIT(&bars.dq_full, it & 1, 0);
+        tc_fence_after();
+        uint32_t v[4][32];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) tmem_ld32(tmem + lane_base + 128 + b * 32, v[b]);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bars.dq_empty);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (DO1 || b >= 2) {  // box b-2 (same half) finished reading its staging
+#ifdef A2D_PROFILE
+            const long long tr0 = clock64();
+#endif
+            if (leader) bulk_wait_read1();
+            named_bar_sync(1, 128);
+#ifdef A2D_PROFILE
+            prof[1] += clock64() - tr0;
+#endif
+          }
+          uint8_t* row = stage + (b & 1) * (D * 128) + d * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4*>(row + ((c ^ (d & 7)) << 4)) =
+                make_float4(__uint_as_float(v[b][4 * c]) * scale, __uint_as_float(v[b][4 * c + 1]) * scale,
+                            __uint_as_float(v[b][4 * c + 2]) * scale, __uint_as_float(v[b][4 * c + 3]) * scale);
+          fence_async_smem();
+          named_bar_sync(1, 128);
+          if (leader) {
+            tma_reduce_add_3d(&p.tm_dq, stage + (b & 1) * (D * 128), qt * BQ + 32 * b, 0, h);
+            bulk_commit();
+          }
+        }
+        if (!DO1 && leader) {
+          bulk_wait_read0();
+          mbar_arrive(&bars.dsbuf_free);  // the softmax may store dS_{i+1}
+        }
+      }
+    }
+    if (leader) bulk_wait0();
+    if (warp == 12) PFLUSH(2);
+  } else if (warp >= 4) {
+    // ------------------------------------------------ P/dS warpgroups
+    regs_inc<144>();
+    const int hq = (warp - 4) / 4;
+    const int wq = warp % 4;
+    const int r = wq * 32 + lane;
+    const int key = key0 + r;
+    const bool key_ok = key < p.Tk;
+    const int kpos = key_ok ? p.k_pos[key] : INT_MAX;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const float sl2 = p.scale_log2;
+    const int* qpos_base = p.q_pos;
+    const int Tq = p.Tq;
+    PSTART();
+    LiveIt li;
+    int it = 0;
+    for (int g = 0; g < p.G; ++g) {
+      li.reset(live_mask, nwords);
+      for (int j = 0; j < n_live; ++j, ++it) {
+        const int qt = li.next();
+        const bool full = (full_mask[qt >> 5] >> (qt & 31)) & 1u;
+        const int qs = it % QST;
+        const uint32_t ph = it & 1;
+        PWAIT(&bars.q_full[qs], (it / QST) & 1, 0);  // stats landed with the Q stage
+        const float* stl = reinterpret_cast<const float*>(smem + kStats) + qs * 2 * BQ;
+        const float* std_ = stl + BQ;
+        PWAIT(&bars.s_full, ph, 1);
+        tc_fence_after();
+        // ---- P (fp32, kept for dS) -> P^T bf16 over the consumed S^T columns
+        float pr[2][32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int q0 = hq * 64 + c * 32;  // query column within the tile
+          uint32_t sr[32];
+          tmem_ld32(tmem + lane_base + q0, sr);
+          tmem_ld_wait();
+          if (full) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(stl + q0 + e);
+              pr[c][e + 0] = ex2(fmaf(__uint_as_float(sr[e + 0]), sl2, -l4.x));
+              pr[c][e + 1] = ex2(fmaf(__uint_as_float(sr[e + 1]), sl2, -l4.y));
+              pr[c][e + 2] = ex2(fmaf(__uint_as_float(sr[e + 2]), sl2, -l4.z));
+              pr[c][e + 3] = ex2(fmaf(__uint_as_float(sr[e + 3]), sl2, -l4.w));
+            }
+          } else {
+            const int qb0 = qt * BQ + q0;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int q = qb0 + e;
+              const int qp = __ldg(qpos_base + min(q, Tq - 1));
+              const bool keep = key_ok && q < Tq && (!causal || kpos <= qp);
+              const float pv = ex2(fmaf(__uint_as_float(sr[e]), sl2, -stl[q0 + e]));
+              pr[c][e] = keep ? pv : 0.f;
+            }
+          }
+          uint32_t pw[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pw[e] = pack_bf16(pr[c][2 * e], pr[c][2 * e + 1]);
+          tmem_st16(tmem + lane_base + q0, pw);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars.p_full);
+        // ---- dS = P (dP - delta) -> dS^T bf16 over the consumed dP^T columns
+        PWAIT(&bars.dp_full, ph, 2);
+        tc_fence_after();
+        uint32_t dw[2][16];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int q0 = hq * 64 + c * 32;
+          uint32_t dr[32];
+          tmem_ld32(tmem + lane_base + 128 + q0, dr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 d4 = *reinterpret_cast<const float4*>(std_ + q0 + e);
+            float ds0 = pr[c][e + 0] * (__uint_as_float(dr[e + 0]) - d4.x);
+            float ds1 = pr[c][e + 1] * (__uint_as_float(dr[e + 1]) - d4.y);
+            float ds2 = pr[c][e + 2] * (__uint_as_float(dr[e + 2]) - d4.z);
+            float ds3 = pr[c][e + 3] * (__uint_as_float(dr[e + 3]) - d4.w);
+            if (!full) {  // masked / padded entries: P = 0 and delta may be stale
+              ds0 = pr[c][e + 0] != 0.f ? ds0 : 0.f;
+              ds1 = pr[c][e + 1] != 0.f ? ds1 : 0.f;
+              ds2 = pr[c][e + 2] != 0.f ? ds2 : 0.f;
+              ds3 = pr[c][e + 3] != 0.f ? ds3 : 0.f;
+            }
+            dw[c][e / 2] = pack_bf16(ds0, ds1);
+            dw[c][e / 2 + 1] = pack_bf16(ds2, ds3);
+          }
+          tmem_st16(tmem + lane_base + 128 + q0, dw[c]);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars.dst_full);
+        // ---- dS^T to shared memory (MN-major B of dQ^T) once the drain of
+        // dQ^T_{i-1} is off the buffer
+        if (!DO1 && it >= 1) PWAIT(&bars.dsbuf_free, (it - 1) & 1, 3);
+        uint8_t* panel = smem + kDS + hq * 16384;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            *reinterpret_cast<uint4*>(panel + sw128_offset(r, 4 * c + m)) =
+                make_uint4(dw[c][4 * m], dw[c][4 * m + 1], dw[c][4 * m + 2], dw[c][4 * m + 3]);
+        fence_async_smem();
+        mbar_arrive(&bars.dss_full);
+      }
+    }
+    if (warp == 4) PFLUSH(1);
+    // ------------------------------------------------ dV (hq=0) / dK (hq=1) epilogue
+    if (n > 0) {
+      mbar_wait(&bars.dkv_full, 0);
+      tc_fence_after();
+    }
+    float* dst = (hq == 0 ? p.dv : p.dk) + ((size_t)hk * p.Tk + key) * D;
+    const float oscale = hq == 0 ? 1.f : p.scale;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t rr[32];
+      if (n > 0) {
+        tmem_ld32(tmem + lane_base + 256 + hq * D + c * 32, rr);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) rr[j] = 0u;
+      }
+      if (key_ok) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 val = make_float4(__uint_as_float(rr[j]) * oscale, __uint_as_float(rr[j + 1]) * oscale,
+                                   __uint_as_float(rr[j + 2]) * oscale, __uint_as_float(rr[j + 3]) * oscale);
+          float4* d4 = reinterpret_cast<float4*>(dst + c * 32 + j);
+          if (p.accumulate_kv) {
+            const float4 o = *d4;
+            val.x += o.x; val.y += o.y; val.z += o.z; val.w += o.w;
+          }
+          *d4 = val;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+template <int D, bool DO1>
+static cudaError_t launch_bwd_q128(const BwdParams& p, cudaStream_t s) {
+  constexpr int bytes = bwd2::Cfg<D, DO1>::kBytes;
+  static_assert(bytes <= 232448, "backward shared memory exceeds 227 KB");
+  cudaError_t e =
+      cudaFuncSetAttribute(fa_bwd_q128_kernel<D, DO1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid((p.Tk + bwd2::BK - 1) / bwd2::BK, p.Hkv);
+  fa_bwd_q128_kernel<D, DO1><<<grid, bwd2::kThreads, bytes, s>>>(p);
+  return cudaGetLastError();
+}

@@ -246,6 +246,13 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   const int n = bars.n_live;
   long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   (void)prof;
+  // register budget: the TMA/MMA/alloc warpgroup hands registers to the two
+  // softmax warpgroups: 88 + 2 x 208 = 504 = the launch allocation (168 x 3
+  // warpgroups; setmaxnreg.inc blocks until the pool has the registers, so
+  // the sum must not exceed it). The increase sits
+  // inside the softmax branch so ptxas allocates that code at 208 (outside
+  // the branch it compiled the softmax at the launch budget and spilled).
+  if (warp < 4) regs_dec<88>();
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     FSTART();
@@ -349,6 +356,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
     FFLUSH(0);
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax
+    regs_inc<208>();
     const int t = (warp - 4) / 4;          // query tile of this warpgroup
     const int wq = warp % 4;               // TMEM lane quarter
     const int row_in_tile = wq * 32 + lane;

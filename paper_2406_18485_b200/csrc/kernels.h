@@ -33,6 +33,8 @@ struct BwdParams {
   CUtensorMap tm_q, tm_k, tm_v, tm_do;  // box {64,64,1} for q/do, {64,128,1} for k/v
   CUtensorMap tm_dq;                    // fp32 dq_acc^T [H][D][Tq_pad], box {32 q,D d,1}, SW128
   CUtensorMap tm_dq8;                   // same tensor, box {8 q,32 d,1}, no swizzle (per-warp drain)
+  float* dq;                            // the same dq_acc^T at this slice's first query (red drain)
+  int dq_ld;                            // its row stride (Tq_pad)
   const int* q_pos;
   const int* k_pos;
   const int2* q_bounds;   // per 64-row query tile

@@ -29,6 +29,14 @@ SLOTS = {
     "drain": ["dq_full(dQ GEMM)", "bulk_wait_read(TMA reduce)", "-", "-", "-", "-", "-", "total"],
     "tma": ["qdo_empty(MMA frees stage)", "-", "-", "-", "-", "-", "-", "total"],
 }
+# the 128-query kernel (fa_bwd_q128.cuh, the D = 128 default; A2D_BWD_VARIANT=6 selects the one above)
+SLOTS_Q128 = {
+    "mma": ["kv_full", "qdo_full(TMA)", "p_full(softmax P)", "dq_empty(drain TMEM read)", "dst_full(softmax dS TMEM)",
+            "dss_full(softmax dS smem)", "do_full(TMA dO)", "total"],
+    "pds": ["qdo_full(stats)", "s_full(MMA S)", "dp_full(MMA dP)", "dsbuf_free(drain staging)", "-", "-", "-", "total"],
+    "drain": ["dq_full(dQ GEMM)", "bulk_wait_read(box b-2)", "-", "-", "-", "-", "-", "total"],
+    "tma": ["q_empty(dK frees Q)", "do_empty(dV frees dO)", "-", "-", "-", "-", "-", "total"],
+}
 FWD_SLOTS = {
     "mma": ["v_full(TMA)", "p_full0(softmax WG0)", "k_full(TMA)", "p_full1(softmax WG1)", "-", "-", "-", "total"],
     "softmax0": ["s_full(MMA QK)", "-", "-", "-", "-", "-", "-", "total"],
@@ -92,10 +100,11 @@ def main():
     lib.a2d_prof_read(buf, 32)
     ms = e0.elapsed_time(e1)
     res = {"shape": vars(a), "bwd_ms": ms, "bwd_tflops": 2.5 * 2.0 * S * S * H * d / ms / 1e9}
+    slots = SLOTS_Q128 if d == 128 and os.environ.get("A2D_BWD_VARIANT", "0") in ("0", "7") else SLOTS
     for role, base in (("mma", 0), ("pds", 8), ("drain", 16), ("tma", 24)):
         vals = list(buf[base:base + 8])
         tot = vals[7] or 1
-        res[role] = {SLOTS[role][i]: round(vals[i] / tot, 4) for i in range(7) if SLOTS[role][i] != "-"}
+        res[role] = {slots[role][i]: round(vals[i] / tot, 4) for i in range(7) if slots[role][i] != "-"}
         res[role]["total_Gcycles"] = vals[7] / 1e9
     print(json.dumps(res, indent=1))
 
