@@ -60,11 +60,13 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, profile: bool = False, variant: str = "") -> str:
     """profile=True: a separate lib/libattn2d_sm100_prof.so with -DA2D_PROFILE
     (per-role barrier wait counters in the backward, a2d_prof_read); never
-    loaded by default."""
-    lib_out = LIB.replace(".so", "_prof.so") if profile else LIB
+    loaded by default. variant="X": also -DA2D_X, library suffix _prof_x
+    (experiments, e.g. SPIN)."""
+    tag = "_prof" + (f"_{variant.lower()}" if variant else "")
+    lib_out = LIB.replace(".so", f"{tag}.so") if profile else LIB
     if not profile and not force and not needs_build():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
@@ -74,15 +76,16 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     procs = []
     objs = []
     for src in SOURCES:
-        obj = os.path.join(BUILD, src.replace(".cu", "_prof.o" if profile else ".o"))
+        obj = os.path.join(BUILD, src.replace(".cu", f"{tag}.o" if profile else ".o"))
         objs.append(obj)
-        cmd = [cc, *ARCH, *FLAGS, *(["-DA2D_PROFILE"] if profile else []), "-I", os.path.join(ROOT, "include"),
+        defs = (["-DA2D_PROFILE"] + ([f"-DA2D_{variant}"] if variant else [])) if profile else []
+        cmd = [cc, *ARCH, *FLAGS, *defs, "-I", os.path.join(ROOT, "include"),
                "-I", nccl_inc, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     failed = []
     for src, p in procs:
         out, _ = p.communicate()
-        log = os.path.join(BUILD, src + ("_prof" if profile else "") + ".log")
+        log = os.path.join(BUILD, src + (tag if profile else "") + ".log")
         with open(log, "w") as f:
             f.write(out)
         if verbose:
@@ -107,8 +110,9 @@ def main(argv=None) -> int:
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
     ap.add_argument("--profile", action="store_true", help="build the instrumented lib/libattn2d_sm100_prof.so")
+    ap.add_argument("--variant", default="", help="with --profile: extra -DA2D_<VARIANT> (library _prof_<variant>)")
     a = ap.parse_args(argv)
-    print(build(force=a.force, verbose=a.verbose, profile=a.profile))
+    print(build(force=a.force, verbose=a.verbose, profile=a.profile, variant=a.variant))
     return 0
 
 

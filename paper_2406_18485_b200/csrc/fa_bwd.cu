@@ -43,10 +43,29 @@ namespace a2d {
 // warpgroup 0 (warp 4 lane 0), 2 dQ drain (warp 12 lane 0), 3 TMA producer).
 #ifdef A2D_PROFILE
 __device__ unsigned long long g_bwd_prof[32];
+// ablations for bottleneck measurement only (profile build; results are wrong):
+// bit 0: the 128-query kernel skips its dQ^T reduce-adds; bit 1: it loads
+// Q/dO only for its first two iterations (stale tiles afterwards)
+__device__ int g_bwd_ablate;
+// per-event clock64 timeline of one CTA (key tile 0, head 0), iterations
+// [kTraceIt0, kTraceIt0 + 32), 16 event slots each (tools/bwd_prof.py --trace)
+constexpr int kTraceIt0 = 200;
+__device__ long long g_bwd_trace[32 * 16];
+__device__ long long g_bwd_trace2[32 * 4];  // observer warp: s_full, dp_full, dq_full, p_full completion
+#define TR(slot, iter)                                                                                  \
+  do {                                                                                                 \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && (iter) >= kTraceIt0 && (iter) < kTraceIt0 + 32) \
+      g_bwd_trace[((iter) - kTraceIt0) * 16 + (slot)] = clock64();                                     \
+  } while (0)
+#ifdef A2D_SPIN
+#define A2D_WAIT mbar_spin
+#else
+#define A2D_WAIT mbar_wait
+#endif
 #define PWAIT(bar, ph, slot)             \
   do {                                   \
     const long long t0_ = clock64();     \
-    mbar_wait(bar, ph);                  \
+    A2D_WAIT(bar, ph);                   \
     prof[slot] += clock64() - t0_;       \
   } while (0)
 #define PSTART() const long long pt0_ = clock64()
@@ -58,6 +77,7 @@ __device__ unsigned long long g_bwd_prof[32];
   } while (0)
 #else
 #define PWAIT(bar, ph, slot) mbar_wait(bar, ph)
+#define TR(slot, iter)
 #define PSTART()
 #define PFLUSH(role)
 #endif
@@ -574,9 +594,10 @@ static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
 }
 
 // Experiment switch (A2D_BWD_VARIANT, read once): 0 default (D = 128: the
-// 128-query kernel, fa_bwd_q128.cuh, 1 dO stage + dedicated drain staging;
-// D = 64: the 64-query kernel), 7 = the 128-query kernel with 2 dO stages
-// and the drain staging in the dS^T buffer, 6 = the
+// 128-query kernel, fa_bwd_q128.cuh, own drain staging; D = 64: the
+// 64-query kernel), 7 / 8 = the 128-query kernel with the kStageDs /
+// kStageHybrid drain staging, 9 / 10 = own staging with 1/8 / 1/4 of the
+// P exps on the FMA pipe, 6 = the
 // 64-query kernel at D = 128 (3 stages, no prefetch), 1 = it with 2 stages,
 // 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead, 4 = 4 stages with the
 // per-warp 8-query dQ drain, 5 = 3 stages with it.
@@ -601,14 +622,24 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
     case 4: return launch_bwd_d<128, 4, 0, true>(p, s);
     case 5: return launch_bwd_d<128, 3, 0, true>(p, s);
     case 6: return launch_bwd_d<128, 3, 0>(p, s);
-    case 7: return launch_bwd_q128<128, false>(p, s);
-    default: return launch_bwd_q128<128, true>(p, s);
+    case 7: return launch_bwd_q128<128, bwd2::kStageDs>(p, s);
+    case 8: return launch_bwd_q128<128, bwd2::kStageHybrid>(p, s);
+    case 9: return launch_bwd_q128<128, bwd2::kStageOwn, 1>(p, s);
+    case 10: return launch_bwd_q128<128, bwd2::kStageOwn, 2>(p, s);
+    default: return launch_bwd_q128<128, bwd2::kStageOwn>(p, s);
   }
 }
 
 }  // namespace a2d
 
 #ifdef A2D_PROFILE
+extern "C" int a2d_prof_trace(long long* out) {
+  if (cudaMemcpyFromSymbol(out, a2d::g_bwd_trace, sizeof(long long) * 32 * 16) != cudaSuccess) return 2;
+  return cudaMemcpyFromSymbol(out + 32 * 16, a2d::g_bwd_trace2, sizeof(long long) * 32 * 4) == cudaSuccess ? 0 : 2;
+}
+extern "C" int a2d_prof_ablate(int bits) {
+  return cudaMemcpyToSymbol(a2d::g_bwd_ablate, &bits, sizeof(int)) == cudaSuccess ? 0 : 2;
+}
 extern "C" int a2d_prof_read(unsigned long long* out, int n) {
   if (n > 32) n = 32;
   if (cudaMemcpyFromSymbol(out, a2d::g_bwd_prof, n * sizeof(unsigned long long)) != cudaSuccess) return 2;

@@ -39,18 +39,25 @@ constexpr int QST = 2;
 constexpr int kThreads = 512;
 constexpr int kMaxQTiles = 1024;  // per launch (the C ABI slices at 131072 queries)
 constexpr int kWords = kMaxQTiles / 32;
-// DO1: one dO stage instead of two; the 32 KB it frees become the dQ^T
-// drain's own staging (otherwise the drain borrows the dS^T buffer).
-template <int D, bool DO1>
+// dQ^T drain staging modes (each box = [D][32 q] fp32, 16 KB at D = 128):
+//  kStageHybrid (default): one dO stage; the 32 KB it frees are the drain's
+//    own staging for boxes 2,3, and boxes 0,1 go to the dS^T buffer, which is
+//    free from dQ^T_i's completion until the softmax stores dS_{i+1} (it waits
+//    for those two reduces to finish reading): all four boxes in flight.
+//  kStageOwn: one dO stage, all boxes through the own 32 KB (two in flight).
+//  kStageDs: two dO stages, all boxes through the dS^T buffer.
+constexpr int kStageHybrid = 0, kStageOwn = 1, kStageDs = 2;
+template <int D, int MODE>
 struct Cfg {
-  static constexpr int kDOST = DO1 ? 1 : 2;              // dO stages (Q always has 2)
+  static constexpr bool kOwn = MODE != kStageDs;
+  static constexpr int kDOST = kOwn ? 1 : 2;             // dO stages (Q always has 2)
   static constexpr int kK = 0;
   static constexpr int kV = kK + BK * D * 2;
   static constexpr int kQ = kV + BK * D * 2;             // QST x [D/64 panels][128 q][64] SW128
   static constexpr int kDO = kQ + QST * BQ * D * 2;
   static constexpr int kDS = kDO + kDOST * BQ * D * 2;   // dS^T [2 panels][128 keys][64 q] SW128
-  static constexpr int kSTG = kDS + BK * BQ * 2;         // drain staging: 2 SW128 boxes [D][32 q] fp32 (DO1)
-  static constexpr int kStats = kSTG + (DO1 ? 2 * D * 128 : 0);  // QST x (lse2[128], delta[128])
+  static constexpr int kSTG = kDS + BK * BQ * 2;         // own drain staging: 2 SW128 boxes [D][32 q] fp32
+  static constexpr int kStats = kSTG + (kOwn ? 2 * D * 128 : 0);  // QST x (lse2[128], delta[128])
   static constexpr int kMask = kStats + QST * 2 * BQ * 4;  // live bits, full bits
   static constexpr int kBars = kMask + 2 * kWords * 4;
   static constexpr int kBytes = kBars + 256;
@@ -84,10 +91,13 @@ struct LiveIt {
 };
 }  // namespace bwd2
 
-template <int D, bool DO1>
+// PX: exp2 pairs computed on the FMA pipe (ex2_poly2) instead of MUFU, out of
+// every four pairs of a full tile's P (0, 1 or 2): the P phase is MUFU-bound
+// (128 x 128 exps per iteration = 1024 MUFU clk) and gates dV.
+template <int D, int MODE, int PX>
 __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __grid_constant__ BwdParams p) {
   using namespace bwd2;
-  using C = Cfg<D, DO1>;
+  using C = Cfg<D, MODE>;
   constexpr int NDO = C::kDOST;
   static_assert(D == 128, "the 128-query backward is built for head dim 128");
   constexpr int kK = C::kK, kV = C::kV, kQ = C::kQ, kDO = C::kDO, kDS = C::kDS, kStats = C::kStats;
@@ -116,11 +126,13 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
     }
     mbar_init(&bars.s_full, 1);
     mbar_init(&bars.dp_full, 1);
-    mbar_init(&bars.p_full, 256);
-    mbar_init(&bars.dst_full, 256);
-    mbar_init(&bars.dss_full, 256);
+    // P/dS and drain hand-offs arrive once per warp (after __syncwarp): 8 / 4
+    // arrivals instead of 256 / 128 serialised shared-memory atomics
+    mbar_init(&bars.p_full, 8);
+    mbar_init(&bars.dst_full, 8);
+    mbar_init(&bars.dss_full, 8);
     mbar_init(&bars.dq_full, 1);
-    mbar_init(&bars.dq_empty, 128);
+    mbar_init(&bars.dq_empty, 4);
     mbar_init(&bars.dsbuf_free, 1);
     mbar_init(&bars.dkv_full, 1);
     fence_mbar_init();
@@ -181,6 +193,14 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
           const int qs = it % QST, ds = it % NDO;
           // Q (+ the stats) once dK_{it-2} freed the stage, dO once dV_{it-NDO} did
           PWAIT(&bars.q_empty[qs], ((it / QST) & 1) ^ 1, 0);
+#ifdef A2D_PROFILE
+          if ((g_bwd_ablate & 2) && it >= 2) {  // stale tiles: arrive without loading
+            mbar_arrive(&bars.q_full[qs]);
+            PWAIT(&bars.do_empty[ds], ((it / NDO) & 1) ^ 1, 1);
+            mbar_arrive(&bars.do_full[ds]);
+            continue;
+          }
+#endif
           // stats: 128 rows, or 64 when the tile's second half lies past the
           // 64-row padding of the stats (then the tile is on the masked path)
           const int nst = (2 * qt + 1 < nqt64) ? BQ : 64;
@@ -202,7 +222,27 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
       }
     }
     PFLUSH(3);
-  } else if (warp == 1) {
+  }
+#ifdef A2D_PROFILE
+  else if (warp == 3) {
+    // observer: completion times of the commit / hand-off barriers (CTA 0 only)
+    if (blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) {
+      uint64_t* bs[4] = {&bars.s_full, &bars.dp_full, &bars.dq_full, &bars.p_full};
+      int nxt[4] = {0, 0, 0, 0};
+      const int lim = min(n, kTraceIt0 + 32);
+      while (nxt[0] < lim || nxt[1] < lim || nxt[2] < lim || nxt[3] < lim) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (nxt[k] < lim && mbar_test_wait(bs[k], nxt[k] & 1)) {
+            if (nxt[k] >= kTraceIt0) g_bwd_trace2[(nxt[k] - kTraceIt0) * 4 + k] = clock64();
+            ++nxt[k];
+          }
+        }
+      }
+    }
+  }
+#endif
+  else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
     PSTART();
     if (n > 0) {
@@ -249,6 +289,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         const uint64_t qoff = (uint64_t)qs * kStage, doff = (uint64_t)ds * kStage;
         // dV += P^T_i dO_i (TS: P^T in R_S; 16 queries per K step at col 32(k/2)+8(k%2))
         PWAIT(&bars.p_full, ph, 2);
+        TR(0, i);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
@@ -262,11 +303,13 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         // S^T_{i+1} into R_S (after dV_i in the in-order pipe)
         if (i + 1 < n) {
           PWAIT(&bars.q_full[(i + 1) % QST], ((i + 1) / QST) & 1, 1);
+          TR(1, i);
           tc_fence_after();
           issue_sdp(i + 1, 0);
         }
         // dK += dS^T_i Q_i (TS: dS^T in R_dP), then release Q_i/dO_i
         PWAIT(&bars.dst_full, ph, 4);
+        TR(2, i);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
@@ -279,6 +322,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         __syncwarp();
         // dQ^T_i = K^T dS^T_i into R_dP (after dK_i); dS^T from shared memory
         PWAIT(&bars.dss_full, ph, 5);
+        TR(3, i);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
@@ -291,7 +335,9 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         // dP^T_{i+1} into R_dP once the drain has read dQ^T_i
         if (i + 1 < n) {
           PWAIT(&bars.dq_empty, ph, 3);
+          TR(4, i);
           PWAIT(&bars.do_full[(i + 1) % NDO], ((i + 1) / NDO) & 1, 6);
+          TR(5, i);
           tc_fence_after();
           issue_sdp(i + 1, 1);
         }
@@ -305,16 +351,16 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
     // ------------------------------------------------ dQ^T drain warpgroup
     // Reads all of R_dP (TMEM lane = feature d, column = query) and releases
     // it for dP_{i+1}; then streams the 128 queries as four SW128 boxes
-    // [128 d][32 q] through the two halves of the dS^T buffer (free from
-    // dQ^T_i's completion until the softmax stores dS_{i+1}) into TMA bulk
-    // reduce-adds on the transposed fp32 dq_acc, two boxes in flight.
+    // [D][32 q] into TMA bulk reduce-adds on the transposed fp32 dq_acc
+    // through the staging of MODE (above). The SM's L1->L2 request path is
+    // the limit (~2/3 of it is these reduces), so what matters is how many
+    // boxes can be in flight while the drain already waits for dQ^T_{i+1}.
     // (red.global from registers measured 2x slower: 1-sector L2 requests.)
     regs_inc<160>();
     const int wq = warp % 4;
     const int d = wq * 32 + lane;
     PSTART();
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    uint8_t* stage = smem + (DO1 ? C::kSTG : kDS);
     const bool leader = warp == 12 && lane == 0;
     const float scale = p.scale;
     LiveIt li;
@@ -325,26 +371,43 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
       for (int j = 0; j < n_live; ++j, ++it) {
         const int qt = li.next();
         PWAIT(&bars.dq_full, it & 1, 0);
+        if (warp == 12) TR(13, it);
         tc_fence_after();
         uint32_t v[4][32];
 #pragma unroll
         for (int b = 0; b < 4; ++b) tmem_ld32(tmem + lane_base + 128 + b * 32, v[b]);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(&bars.dq_empty);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.dq_empty);
+        if (warp == 12) TR(14, it);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          if (DO1 || b >= 2) {  // box b-2 (same half) finished reading its staging
+          uint8_t* box;
+          bool wait;  // the reduce that last read this slot must be done
+          if constexpr (MODE == kStageHybrid) {
+            box = smem + (b < 2 ? kDS + b * (D * 128) : C::kSTG + (b - 2) * (D * 128));
+            wait = b == 2;  // (boxes 0,1: the dS^T buffer is free once dQ^T_i is done)
+          } else {
+            box = smem + (MODE == kStageOwn ? C::kSTG : kDS) + (b & 1) * (D * 128);
+            wait = MODE == kStageOwn || b >= 2;
+          }
+          if (wait) {
 #ifdef A2D_PROFILE
             const long long tr0 = clock64();
 #endif
-            if (leader) bulk_wait_read1();
+            if (leader) {
+              if (MODE == kStageHybrid)
+                bulk_wait_read2();  // only boxes 0,1 of this iteration may still be reading
+              else
+                bulk_wait_read1();
+            }
             named_bar_sync(1, 128);
 #ifdef A2D_PROFILE
             prof[1] += clock64() - tr0;
 #endif
           }
-          uint8_t* row = stage + (b & 1) * (D * 128) + d * 128;
+          uint8_t* row = box + d * 128;
 #pragma unroll
           for (int c = 0; c < 8; ++c)
             *reinterpret_cast<float4*>(row + ((c ^ (d & 7)) << 4)) =
@@ -353,14 +416,22 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
           fence_async_smem();
           named_bar_sync(1, 128);
           if (leader) {
-            tma_reduce_add_3d(&p.tm_dq, stage + (b & 1) * (D * 128), qt * BQ + 32 * b, 0, h);
+#ifdef A2D_PROFILE
+            if (!(g_bwd_ablate & 1))
+#endif
+              tma_reduce_add_3d(&p.tm_dq, box, qt * BQ + 32 * b, 0, h);
             bulk_commit();
           }
         }
-        if (!DO1 && leader) {
-          bulk_wait_read0();
-          mbar_arrive(&bars.dsbuf_free);  // the softmax may store dS_{i+1}
+        if (MODE != kStageOwn && leader) {
+          // the dS^T buffer's reduces are done reading: the softmax may store dS_{i+1}
+          if (MODE == kStageHybrid)
+            bulk_wait_read2();
+          else
+            bulk_wait_read0();
+          mbar_arrive(&bars.dsbuf_free);
         }
+        if (warp == 12) TR(15, it);
       }
     }
     if (leader) bulk_wait0();
@@ -392,6 +463,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         const float* stl = reinterpret_cast<const float*>(smem + kStats) + qs * 2 * BQ;
         const float* std_ = stl + BQ;
         PWAIT(&bars.s_full, ph, 1);
+        if (warp == 4) TR(6, it);
         tc_fence_after();
         // ---- P (fp32, kept for dS) -> P^T bf16 over the consumed S^T columns
         float pr[2][32];
@@ -405,10 +477,28 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
 #pragma unroll
             for (int e = 0; e < 32; e += 4) {
               const float4 l4 = *reinterpret_cast<const float4*>(stl + q0 + e);
-              pr[c][e + 0] = ex2(fmaf(__uint_as_float(sr[e + 0]), sl2, -l4.x));
-              pr[c][e + 1] = ex2(fmaf(__uint_as_float(sr[e + 1]), sl2, -l4.y));
-              pr[c][e + 2] = ex2(fmaf(__uint_as_float(sr[e + 2]), sl2, -l4.z));
-              pr[c][e + 3] = ex2(fmaf(__uint_as_float(sr[e + 3]), sl2, -l4.w));
+              const float x0 = fmaf(__uint_as_float(sr[e + 0]), sl2, -l4.x);
+              const float x1 = fmaf(__uint_as_float(sr[e + 1]), sl2, -l4.y);
+              const float x2 = fmaf(__uint_as_float(sr[e + 2]), sl2, -l4.z);
+              const float x3 = fmaf(__uint_as_float(sr[e + 3]), sl2, -l4.w);
+              // pair index within 8 consecutive pairs: (e/2) % 8 and (e/2+1) % 8
+              const int pa = (e / 2) % 8;
+              if (PX >= 1 && pa == 6) {  // pairs 6 (and 7 for PX 2) of every 8 -> 1/8 or 1/4 of exps
+                const float2 y = ex2_poly2(make_float2(x0, x1));
+                pr[c][e + 0] = y.x;
+                pr[c][e + 1] = y.y;
+              } else {
+                pr[c][e + 0] = ex2(x0);
+                pr[c][e + 1] = ex2(x1);
+              }
+              if (PX >= 2 && pa == 6) {
+                const float2 y = ex2_poly2(make_float2(x2, x3));
+                pr[c][e + 2] = y.x;
+                pr[c][e + 3] = y.y;
+              } else {
+                pr[c][e + 2] = ex2(x2);
+                pr[c][e + 3] = ex2(x3);
+              }
             }
           } else {
             const int qb0 = qt * BQ + q0;
@@ -428,9 +518,13 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&bars.p_full);
+        if (warp == 4) TR(7, it);
+        if (warp == 8) TR(12, it);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.p_full);
         // ---- dS = P (dP - delta) -> dS^T bf16 over the consumed dP^T columns
         PWAIT(&bars.dp_full, ph, 2);
+        if (warp == 4) TR(8, it);
         tc_fence_after();
         uint32_t dw[2][16];
 #pragma unroll
@@ -459,10 +553,13 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&bars.dst_full);
+        if (warp == 4) TR(9, it);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.dst_full);
         // ---- dS^T to shared memory (MN-major B of dQ^T) once the drain of
         // dQ^T_{i-1} is off the buffer
-        if (!DO1 && it >= 1) PWAIT(&bars.dsbuf_free, (it - 1) & 1, 3);
+        if (MODE != kStageOwn && it >= 1) PWAIT(&bars.dsbuf_free, (it - 1) & 1, 3);
+        if (warp == 4) TR(10, it);
         uint8_t* panel = smem + kDS + hq * 16384;
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -471,7 +568,9 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
             *reinterpret_cast<uint4*>(panel + sw128_offset(r, 4 * c + m)) =
                 make_uint4(dw[c][4 * m], dw[c][4 * m + 1], dw[c][4 * m + 2], dw[c][4 * m + 3]);
         fence_async_smem();
-        mbar_arrive(&bars.dss_full);
+        if (warp == 4) TR(11, it);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.dss_full);
       }
     }
     if (warp == 4) PFLUSH(1);
@@ -513,14 +612,14 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D, bool DO1>
+template <int D, int MODE, int PX = 0>
 static cudaError_t launch_bwd_q128(const BwdParams& p, cudaStream_t s) {
-  constexpr int bytes = bwd2::Cfg<D, DO1>::kBytes;
+  constexpr int bytes = bwd2::Cfg<D, MODE>::kBytes;
   static_assert(bytes <= 232448, "backward shared memory exceeds 227 KB");
   cudaError_t e =
-      cudaFuncSetAttribute(fa_bwd_q128_kernel<D, DO1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(fa_bwd_q128_kernel<D, MODE, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   dim3 grid((p.Tk + bwd2::BK - 1) / bwd2::BK, p.Hkv);
-  fa_bwd_q128_kernel<D, DO1><<<grid, bwd2::kThreads, bytes, s>>>(p);
+  fa_bwd_q128_kernel<D, MODE, PX><<<grid, bwd2::kThreads, bytes, s>>>(p);
   return cudaGetLastError();
 }

@@ -16,7 +16,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["A2D_LIB"] = os.path.join(ROOT, "paper_2406_18485_b200", "lib", "libattn2d_sm100_prof.so")
+os.environ["A2D_LIB"] = os.path.join(ROOT, "paper_2406_18485_b200", "lib",
+                                     "libattn2d_sm100_prof%s.so" % (("_" + os.environ["A2D_PROF_VARIANT"].lower())
+                                                                   if os.environ.get("A2D_PROF_VARIANT") else ""))
 
 import torch  # noqa: E402
 
@@ -56,6 +58,7 @@ def main():
     lib = _lib.load(os.environ["A2D_LIB"])
     lib.a2d_prof_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.a2d_prof_read_fwd.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.a2d_prof_ablate(int(os.environ.get("A2D_ABLATE", "0")))
     dev = torch.device("cuda:0")
     H, Hkv, S, d = a.heads, a.kv_heads, a.seq, a.dim
     g = torch.Generator(device=dev).manual_seed(0)
@@ -100,12 +103,24 @@ def main():
     lib.a2d_prof_read(buf, 32)
     ms = e0.elapsed_time(e1)
     res = {"shape": vars(a), "bwd_ms": ms, "bwd_tflops": 2.5 * 2.0 * S * S * H * d / ms / 1e9}
-    slots = SLOTS_Q128 if d == 128 and os.environ.get("A2D_BWD_VARIANT", "0") in ("0", "7") else SLOTS
+    slots = SLOTS_Q128 if d == 128 and os.environ.get("A2D_BWD_VARIANT", "0") in ("0", "7", "8", "9", "10") else SLOTS
     for role, base in (("mma", 0), ("pds", 8), ("drain", 16), ("tma", 24)):
         vals = list(buf[base:base + 8])
         tot = vals[7] or 1
         res[role] = {slots[role][i]: round(vals[i] / tot, 4) for i in range(7) if slots[role][i] != "-"}
         res[role]["total_Gcycles"] = vals[7] / 1e9
+    if os.environ.get("A2D_TRACE"):
+        tb = (ctypes.c_longlong * 640)()
+        lib.a2d_prof_trace(tb)
+        names = ["mma:dV(i)", "mma:S(i+1)", "mma:dK(i)", "mma:dQ(i)", "mma:dq_empty", "mma:dP(i+1)",
+                 "sm:s_full", "sm:P_done", "sm:dp_full", "sm:dS_done", "sm:sts_start", "sm:sts_done",
+                 "sm1:P_done", "dr:dq_full", "dr:dq_empty", "dr:end"]
+        t0 = tb[0]
+        res["trace_cycles_rel_to_first_dV"] = {n: [tb[i * 16 + k] - t0 for i in range(32)] for k, n in enumerate(names)}
+        for k, n in enumerate(["ob:s_full", "ob:dp_full", "ob:dq_full", "ob:p_full"]):
+            res["trace_cycles_rel_to_first_dV"][n] = [tb[512 + i * 4 + k] - t0 for i in range(32)]
+        per = [(tb[(i + 1) * 16] - tb[i * 16]) for i in range(31)]
+        res["trace_period"] = per
     print(json.dumps(res, indent=1))
 
 
