@@ -593,11 +593,10 @@ static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Experiment switch (A2D_BWD_VARIANT, read once): 0 default (D = 128: the
-// 128-query kernel, fa_bwd_q128.cuh, own drain staging; D = 64: the
-// 64-query kernel), 7 / 8 = the 128-query kernel with the kStageDs /
+// Experiment switch (A2D_BWD_VARIANT, read once): 0 default (the 128-query
+// kernel, fa_bwd_q128.cuh, own drain staging, D = 64 or 128), 7 / 8 = the 128-query kernel with the kStageDs /
 // kStageHybrid drain staging, 9 / 10 = own staging with 1/8 / 1/4 of the
-// P exps on the FMA pipe, 6 = the
+// P exps on the FMA pipe, 6 = the round-2
 // 64-query kernel at D = 128 (3 stages, no prefetch), 1 = it with 2 stages,
 // 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead, 4 = 4 stages with the
 // per-warp 8-query dQ drain, 5 = 3 stages with it.
@@ -614,7 +613,8 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
   if (head_dim != 128 && head_dim != 64) return cudaErrorInvalidValue;
   if (p.Tk <= 0 || p.Hkv <= 0) return cudaSuccess;
   if ((p.Tq + bwd::BQ - 1) / bwd::BQ > bwd::kMaxQTiles) return cudaErrorInvalidValue;
-  if (head_dim == 64) return launch_bwd_d<64, 3, 0>(p, s);
+  if (head_dim == 64)
+    return bwd_variant() == 6 ? launch_bwd_d<64, 3, 0>(p, s) : launch_bwd_q128<64, bwd2::kStageOwn>(p, s);
   switch (bwd_variant()) {
     case 1: return launch_bwd_d<128, 2, 0>(p, s);
     case 2: return launch_bwd_d<128, 3, 4>(p, s);

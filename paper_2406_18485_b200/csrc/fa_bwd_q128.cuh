@@ -1,4 +1,4 @@
-// K3, round-3 structure: 128-query iterations, every GEMM at N = 128.
+// K3, round-2b structure: 128-query iterations, every GEMM at N = 128.
 // (Included by fa_bwd.cu; shares its wait-time instrumentation.)
 //
 // Same math as fa_bwd_kernel (ref oracle.py:127-152): P = exp(S - LSE),
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
   using namespace bwd2;
   using C = Cfg<D, MODE>;
   constexpr int NDO = C::kDOST;
-  static_assert(D == 128, "the 128-query backward is built for head dim 128");
+  static_assert(D == 128 || D == 64, "head dim 64 or 128");
   constexpr int kK = C::kK, kV = C::kV, kQ = C::kQ, kDO = C::kDO, kDS = C::kDS, kStats = C::kStats;
   extern __shared__ __align__(1024) uint8_t smem[];
   Bars& bars = *reinterpret_cast<Bars*>(smem + C::kBars);
@@ -248,11 +248,14 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
     if (n > 0) {
       constexpr uint32_t id_s = idesc_bf16(BK, BQ, false, false);  // S^T, dP^T: M=128 keys, N=128 q
       constexpr uint32_t id_kv = idesc_bf16(BK, D, false, true);   // dV, dK: TS, B MN-major
-      constexpr uint32_t id_dq = idesc_bf16(D, BQ, true, true);    // dQ^T: M=d, N=128 q
+      // dQ^T: M = 128 feature rows always (for D = 64 rows >= 64 read the next
+      // smem panel and land in TMEM lanes the drain never reads; M = 64 would
+      // cost the same tensor time)
+      constexpr uint32_t id_dq = idesc_bf16(128, BQ, true, true);
       const uint32_t sK = smem_u32(smem + kK), sV = smem_u32(smem + kV);
       const uint32_t sQ = smem_u32(smem + kQ), sDO = smem_u32(smem + kDO);
       const uint32_t sDS = smem_u32(smem + kDS);
-      const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+      const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
       const uint64_t dK0 = sdesc_sw128(sK, 16, 1024), dV0 = sdesc_sw128(sV, 16, 1024);
       const uint64_t dQ0 = sdesc_sw128(sQ, 16, 1024), dDO0 = sdesc_sw128(sDO, 16, 1024);
       const uint64_t dKmn = sdesc_sw128(sK, 16384, 1024);   // K as MN-major A (M = d) of dQ^T
@@ -359,6 +362,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
     regs_inc<160>();
     const int wq = warp % 4;
     const int d = wq * 32 + lane;
+    const bool d_warp_ok = wq * 32 < D;
     PSTART();
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const bool leader = warp == 12 && lane == 0;
@@ -374,9 +378,11 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         if (warp == 12) TR(13, it);
         tc_fence_after();
         uint32_t v[4][32];
+        if (d_warp_ok) {  // (D = 64: warps 14-15 hold no feature rows)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) tmem_ld32(tmem + lane_base + 128 + b * 32, v[b]);
-        tmem_ld_wait();
+          for (int b = 0; b < 4; ++b) tmem_ld32(tmem + lane_base + 128 + b * 32, v[b]);
+          tmem_ld_wait();
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.dq_empty);
@@ -408,11 +414,13 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
 #endif
           }
           uint8_t* row = box + d * 128;
+          if (d_warp_ok) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<float4*>(row + ((c ^ (d & 7)) << 4)) =
-                make_float4(__uint_as_float(v[b][4 * c]) * scale, __uint_as_float(v[b][4 * c + 1]) * scale,
-                            __uint_as_float(v[b][4 * c + 2]) * scale, __uint_as_float(v[b][4 * c + 3]) * scale);
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4*>(row + ((c ^ (d & 7)) << 4)) =
+                  make_float4(__uint_as_float(v[b][4 * c]) * scale, __uint_as_float(v[b][4 * c + 1]) * scale,
+                              __uint_as_float(v[b][4 * c + 2]) * scale, __uint_as_float(v[b][4 * c + 3]) * scale);
+          }
           fence_async_smem();
           named_bar_sync(1, 128);
           if (leader) {

@@ -29,8 +29,8 @@ class B200Calibration:
     """Measured on B200 (round 1): tools/kbench.py, bench.py sweeps, tools/trace.py
     phase traces (profiles/r01_trace_*.json), guide peaks."""
 
-    fwd_tflops: float = 1180.0     # forward chunk kernel in a full step (final round-1 build)
-    bwd_tflops: float = 1040.0     # backward chunk kernel in a full step (final round-1 build)
+    fwd_tflops: float = 1195.0     # forward chunk kernel in a full step (round-2b build)
+    bwd_tflops: float = 1110.0     # backward chunk kernel in a full step (round-2b 128-query kernel)
     short_chunk_tokens: float = 500.0   # kernel efficiency ~ C / (C + this) for small chunks
     a2a_gbs: float = 620.0         # NCCL all_to_all_single: time ~ whole buffer / this (traces, d_hp = 2 and 4)
     ce_gbs: float = 770.0          # copy-engine write into a peer's symmetric buffer (tools/probes/peer_probe.py)
@@ -51,6 +51,9 @@ def calibration() -> B200Calibration:
 # The earlier round-1 build that produced profiles/r01_sweep_*.jsonl (NCCL
 # all-to-all, backward before the transposed-dQ drain).
 EARLY_ROUND1 = B200Calibration(fwd_tflops=1100.0, bwd_tflops=940.0, transport="nccl")
+# The final round-1 / round-2 builds (64-query backward) that produced
+# profiles/r01_final_sweep_S128k_symm_2_4gpu.jsonl.
+ROUND2 = B200Calibration(fwd_tflops=1180.0, bwd_tflops=1040.0)
 
 
 def _eff(c: B200Calibration, tokens: int) -> float:

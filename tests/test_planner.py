@@ -12,18 +12,19 @@ from paper_2406_18485_b200.config import ModelConfig, ParallelConfig, Placement
 # (sweep, calibration of the build that produced it, expected row count)
 SWEEPS = [(os.path.join(ROOT, "profiles", "r01_sweep_S128k_2_4gpu.jsonl"), P.EARLY_ROUND1, 18),
           (os.path.join(ROOT, "profiles", "r01_sweep_S512k_2_4gpu.jsonl"), P.EARLY_ROUND1, 18),
-          (os.path.join(ROOT, "profiles", "r01_final_sweep_S128k_symm_2_4gpu.jsonl"), P.calibration(), 9)]
+          (os.path.join(ROOT, "profiles", "r01_final_sweep_S128k_symm_2_4gpu.jsonl"), P.ROUND2, 9),
+          (os.path.join(ROOT, "profiles", "r02b_sweep_S128k_4gpu.jsonl"), P.calibration(), 6)]
 REF_SRC = os.environ.get("ATTN2D_REF", "/root/reference/pkg/src")
 
 
-@pytest.mark.parametrize("path,cal,rows", SWEEPS, ids=["S128k", "S512k", "S128k_final"])
+@pytest.mark.parametrize("path,cal,rows", SWEEPS, ids=["S128k", "S512k", "S128k_final", "S128k_r02b"])
 def test_predictions_track_measured_sweeps(path, cal, rows):
     r = P.check_against_sweep(path, cal)
     assert r["n"] == rows
     assert r["mean_rel_err"] < 0.08 and r["max_rel_err"] < 0.15, r
 
 
-@pytest.mark.parametrize("path,cal,rows", SWEEPS, ids=["S128k", "S512k", "S128k_final"])
+@pytest.mark.parametrize("path,cal,rows", SWEEPS, ids=["S128k", "S512k", "S128k_final", "S128k_r02b"])
 def test_planner_pick_is_near_measured_best(path, cal, rows):
     import json
     groups = {}

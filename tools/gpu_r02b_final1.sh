@@ -1,4 +1,4 @@
-# 1 GPU, round-3 build evidence (128-query backward): smoke, the whole -m gpu suite (1-GPU cases),
+# 1 GPU, round-2b build evidence (128-query backward): smoke, the whole -m gpu suite (1-GPU cases),
 # the default bench (N=1, parity check on), BASELINE config 1/2 shapes, the
 # native runtime, then the ncu launch list (with DRAM bytes) of the bench
 # command and one ncu --set full capture of each attention kernel.

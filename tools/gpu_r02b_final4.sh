@@ -1,4 +1,4 @@
-# 4 GPUs, round-3 build evidence (128-query backward): the whole -m gpu suite (1/2/4-rank cases),
+# 4 GPUs, round-2b build evidence (128-query backward): the whole -m gpu suite (1/2/4-rank cases),
 # bench N=2 / N=4 (python and native runtimes), the S=128K factorisation sweep
 # (head-first; placements only renumber ranks on one node, both are in the
 # suite), config-4-like GQA S=256K, and config 1 on its own 2x2 w=2 grid.
