@@ -26,6 +26,8 @@
 #include "sm100.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace a2d {
 
 // Optional wait-time instrumentation (-DA2D_PROFILE, build.py --profile):
@@ -76,7 +78,7 @@ struct FwdBars {
   uint64_t q_full;
   uint64_t k_full[fwd::KST], k_empty[fwd::KST];
   uint64_t v_full[fwd::VST], v_empty[fwd::VST];
-  uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t s_full[2], p_half[2], p_full[2], o_full[2];
   uint32_t tmem_base;
   int n_live;
   int warp_cnt[12];
@@ -195,7 +197,10 @@ __device__ __forceinline__ void fwd_epilogue(const FwdParams& p, uint32_t tO, in
   }
 }
 
-template <int D>
+// SPLIT: the softmax releases P in two halves (keys 0-63, then 64-127) so the
+// first half of PV starts while it still computes the second (PV's K steps
+// run over keys); the O rescale moves before the exps to keep that legal.
+template <int D, bool SPLIT>
 __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_constant__ FwdParams p) {
   using namespace fwd;
   using L = FwdSmem<D>;
@@ -224,6 +229,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
     for (int i = 0; i < VST; ++i) { mbar_init(&bars.v_full[i], 1); mbar_init(&bars.v_empty[i], 1); }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars.s_full[t], 1);
+      mbar_init(&bars.p_half[t], 128);
       mbar_init(&bars.p_full[t], 128);
       mbar_init(&bars.o_full[t], 1);
     }
@@ -299,9 +305,9 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
                   dK0 + (uint64_t)((ks * L::kTileBytes) >> 4) + off, id_qk, k > 0);
         }
       };
-      auto issue_pv = [&](int t, int vs, bool acc) {
+      auto issue_pv = [&](int t, int vs, bool acc, int k0, int k1) {
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k)
+        for (int k = k0; k < k1; ++k)
           umma_ts(tO[t], tS[t] + k * 8, dV0 + (uint64_t)((vs * L::kTileBytes) >> 4) + (uint64_t)(k * 128), id_pv,
                   (acc || k > 0) ? 1u : 0u);
       };
@@ -322,12 +328,19 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         FWAIT(&bars.v_full[vs], (it / VST) & 1, 0);
         const bool more = it + 1 < n;
         const int ks1 = (it + 1) % KST;
+        if (SPLIT) {  // keys 0-63 of P_0 while the softmax still produces 64-127
+          FWAIT(&bars.p_half[0], it & 1, 1);
+          tc_fence_after();
+          __syncwarp();
+          if (elect_one()) issue_pv(0, vs, it > 0, 0, BN / 32);
+          __syncwarp();
+        }
         FWAIT(&bars.p_full[0], it & 1, 1);
         if (more) FWAIT(&bars.k_full[ks1], ((it + 1) / KST) & 1, 2);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
-          issue_pv(0, vs, it > 0);
+          issue_pv(0, vs, it > 0, SPLIT ? BN / 32 : 0, BN / 16);
           if (more) {
             issue_qk(0, ks1);
             umma_commit(&bars.s_full[0]);
@@ -336,11 +349,18 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           }
         }
         __syncwarp();
+        if (SPLIT) {
+          FWAIT(&bars.p_half[1], it & 1, 3);
+          tc_fence_after();
+          __syncwarp();
+          if (elect_one()) issue_pv(1, vs, it > 0, 0, BN / 32);
+          __syncwarp();
+        }
         FWAIT(&bars.p_full[1], it & 1, 3);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
-          issue_pv(1, vs, it > 0);
+          issue_pv(1, vs, it > 0, SPLIT ? BN / 32 : 0, BN / 16);
           umma_commit(&bars.v_empty[vs]);
           if (more) {
             issue_qk(1, ks1);
@@ -426,6 +446,19 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         m_used = m_tile;
         l_sum *= alpha;
       }
+      if (__any_sync(0xffffffffu, rescale)) {
+        // O (this tile's previous PV) is complete: s_full's commit tracks it.
+        // Rescaled before P is released (SPLIT lets PV start on half of P).
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st32(tO + c * 32, r);
+        }
+      }
       const float neg_m = m_used == -INFINITY ? 0.f : -m_used;
       const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
       float2 part[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -448,23 +481,16 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           pk[(c - cc) / 2] = pack_bf16(e.x, e.y);
         }
         tmem_st16(tS + cc / 2, pk);
+        if (SPLIT && cc == BN / 2 - 32) {  // keys [0, BN/2) of P are in TMEM (and O is rescaled)
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bars.p_half[t]);
+        }
       }
       {
         const float2 p01 = __fadd2_rn(part[0], part[1]), p23 = __fadd2_rn(part[2], part[3]);
         const float2 pt = __fadd2_rn(p01, p23);
         l_sum += pt.x + pt.y;
-      }
-      if (__any_sync(0xffffffffu, rescale)) {
-        // O (this tile's previous PV) is complete: s_full's commit tracks it.
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tO + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st32(tO + c * 32, r);
-        }
       }
       tmem_st_wait();
       tc_fence_before();
@@ -487,22 +513,34 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D>
+template <int D, bool SPLIT>
 static cudaError_t launch_fwd_d(const FwdParams& p, cudaStream_t s) {
   if ((p.Tk + fwd::BN - 1) / fwd::BN > fwd::kMaxKTiles) return cudaErrorInvalidValue;
   const int smem = FwdSmem<D>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int nqb = (p.Tq + 255) / 256;
   dim3 grid(nqb, p.H);
-  fa_fwd_kernel<D><<<grid, fwd::kThreads, smem, s>>>(p);
+  fa_fwd_kernel<D, SPLIT><<<grid, fwd::kThreads, smem, s>>>(p);
   return cudaGetLastError();
+}
+
+// Experiment switch (A2D_FWD_VARIANT, read once): 0 default (P released in
+// two halves), 1 = P released once (round 2).
+static int fwd_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("A2D_FWD_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s) {
   if (p.Tq <= 0 || p.H <= 0) return cudaSuccess;
-  if (head_dim == 128) return launch_fwd_d<128>(p, s);
-  if (head_dim == 64) return launch_fwd_d<64>(p, s);
+  const bool split = fwd_variant() != 1;
+  if (head_dim == 128) return split ? launch_fwd_d<128, true>(p, s) : launch_fwd_d<128, false>(p, s);
+  if (head_dim == 64) return split ? launch_fwd_d<64, true>(p, s) : launch_fwd_d<64, false>(p, s);
   return cudaErrorInvalidValue;
 }
 

@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
     ap.add_argument("--timeout", type=int, default=600)
     ap.add_argument("--placements", nargs="+", default=["head_first", "context_first"])
+    ap.add_argument("--bench-args", default="", help="extra bench.py arguments, e.g. '--no-check'")
     a = ap.parse_args()
     model = ModelConfig(seq_len=a.seq, heads=a.heads, kv_heads=a.kv_heads, hidden=a.heads * 128)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
@@ -56,7 +57,8 @@ def main():
                        "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
                        "--gpus", str(n), "--steps", str(a.steps), "--warmup", str(a.warmup), "--seq", str(a.seq),
                        "--heads", str(a.heads), "--kv-heads", str(a.kv_heads), "--d-hp", str(d_hp),
-                       "--d-cp", str(d_cp), "--w", str(w), "--placement", pl, "--no-e2e", "--no-cpu"]
+                       "--d-cp", str(d_cp), "--w", str(w), "--placement", pl, "--no-e2e", "--no-cpu",
+                       *a.bench_args.split()]
                 try:
                     r = subprocess.run(cmd, capture_output=True, text=True, timeout=a.timeout, cwd=ROOT)
                     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
