@@ -596,7 +596,7 @@ static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
 // Experiment switch (A2D_BWD_VARIANT, read once): 0 default (the 128-query
 // kernel, fa_bwd_q128.cuh, own drain staging, D = 64 or 128), 7 / 8 = the 128-query kernel with the kStageDs /
 // kStageHybrid drain staging, 9 / 10 = own staging with 1/8 / 1/4 of the
-// P exps on the FMA pipe, 6 = the round-2
+// P exps on the FMA pipe, 11 = P^T / dS^T released in two parts, 6 = the round-2
 // 64-query kernel at D = 128 (3 stages, no prefetch), 1 = it with 2 stages,
 // 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead, 4 = 4 stages with the
 // per-warp 8-query dQ drain, 5 = 3 stages with it.
@@ -626,6 +626,7 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
     case 8: return launch_bwd_q128<128, bwd2::kStageHybrid>(p, s);
     case 9: return launch_bwd_q128<128, bwd2::kStageOwn, 1>(p, s);
     case 10: return launch_bwd_q128<128, bwd2::kStageOwn, 2>(p, s);
+    case 11: return launch_bwd_q128<128, bwd2::kStageOwn, 0, 1>(p, s);
     default: return launch_bwd_q128<128, bwd2::kStageOwn>(p, s);
   }
 }

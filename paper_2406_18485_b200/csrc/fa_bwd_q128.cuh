@@ -68,6 +68,7 @@ struct Bars {
   uint64_t kv_full;
   uint64_t q_full[QST], q_empty[QST], do_full[QST], do_empty[QST];
   uint64_t s_full, dp_full, p_full, dst_full, dss_full, dq_full, dq_empty, dsbuf_free, dkv_full;
+  uint64_t p_part, dst_part;
   uint32_t tmem_base;
 };
 static_assert(sizeof(Bars) <= 256, "barrier block");
@@ -94,7 +95,9 @@ struct LiveIt {
 // PX: exp2 pairs computed on the FMA pipe (ex2_poly2) instead of MUFU, out of
 // every four pairs of a full tile's P (0, 1 or 2): the P phase is MUFU-bound
 // (128 x 128 exps per iteration = 1024 MUFU clk) and gates dV.
-template <int D, int MODE, int PX>
+// SPL: the P/dS warps release P^T and dS^T in two parts (their first 32-query
+// chunk, then the second), so dV / dK start on half of the K steps early.
+template <int D, int MODE, int PX, int SPL>
 __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __grid_constant__ BwdParams p) {
   using namespace bwd2;
   using C = Cfg<D, MODE>;
@@ -129,6 +132,8 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
     // P/dS and drain hand-offs arrive once per warp (after __syncwarp): 8 / 4
     // arrivals instead of 256 / 128 serialised shared-memory atomics
     mbar_init(&bars.p_full, 8);
+    mbar_init(&bars.p_part, 8);
+    mbar_init(&bars.dst_part, 8);
     mbar_init(&bars.dst_full, 8);
     mbar_init(&bars.dss_full, 8);
     mbar_init(&bars.dq_full, 1);
@@ -291,6 +296,20 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         const uint32_t ph = i & 1;
         const uint64_t qoff = (uint64_t)qs * kStage, doff = (uint64_t)ds * kStage;
         // dV += P^T_i dO_i (TS: P^T in R_S; 16 queries per K step at col 32(k/2)+8(k%2))
+        // (SPL: K steps {0,1,4,5} = the first chunk of both warpgroups, then {2,3,6,7})
+        if (SPL) {
+          PWAIT(&bars.p_part, ph, 2);
+          tc_fence_after();
+          __syncwarp();
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BQ / 16; ++k)
+              if ((k / 2) % 2 == 0)
+                umma_ts(tDV, tS + (k / 2) * 32 + (k % 2) * 8, dDOmn + doff + (uint64_t)(k * 128), id_kv,
+                        (i > 0 || k > 0) ? 1u : 0u);
+          }
+          __syncwarp();
+        }
         PWAIT(&bars.p_full, ph, 2);
         TR(0, i);
         tc_fence_after();
@@ -298,8 +317,9 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BQ / 16; ++k)
-            umma_ts(tDV, tS + (k / 2) * 32 + (k % 2) * 8, dDOmn + doff + (uint64_t)(k * 128), id_kv,
-                    (i > 0 || k > 0) ? 1u : 0u);
+            if (!SPL || (k / 2) % 2 == 1)
+              umma_ts(tDV, tS + (k / 2) * 32 + (k % 2) * 8, dDOmn + doff + (uint64_t)(k * 128), id_kv,
+                      (i > 0 || k > 0) ? 1u : 0u);
           umma_commit(&bars.do_empty[ds]);  // dO_i's last reader
         }
         __syncwarp();
@@ -311,6 +331,19 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
           issue_sdp(i + 1, 0);
         }
         // dK += dS^T_i Q_i (TS: dS^T in R_dP), then release Q_i/dO_i
+        if (SPL) {
+          PWAIT(&bars.dst_part, ph, 4);
+          tc_fence_after();
+          __syncwarp();
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BQ / 16; ++k)
+              if ((k / 2) % 2 == 0)
+                umma_ts(tDK, tDP + (k / 2) * 32 + (k % 2) * 8, dQmn + qoff + (uint64_t)(k * 128), id_kv,
+                        (i > 0 || k > 0) ? 1u : 0u);
+          }
+          __syncwarp();
+        }
         PWAIT(&bars.dst_full, ph, 4);
         TR(2, i);
         tc_fence_after();
@@ -318,8 +351,9 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BQ / 16; ++k)
-            umma_ts(tDK, tDP + (k / 2) * 32 + (k % 2) * 8, dQmn + qoff + (uint64_t)(k * 128), id_kv,
-                    (i > 0 || k > 0) ? 1u : 0u);
+            if (!SPL || (k / 2) % 2 == 1)
+              umma_ts(tDK, tDP + (k / 2) * 32 + (k % 2) * 8, dQmn + qoff + (uint64_t)(k * 128), id_kv,
+                      (i > 0 || k > 0) ? 1u : 0u);
           umma_commit(&bars.q_empty[qs]);
         }
         __syncwarp();
@@ -523,6 +557,12 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
 #pragma unroll
           for (int e = 0; e < 16; ++e) pw[e] = pack_bf16(pr[c][2 * e], pr[c][2 * e + 1]);
           tmem_st16(tmem + lane_base + q0, pw);
+          if (SPL && c == 0) {
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars.p_part);
+          }
         }
         tmem_st_wait();
         tc_fence_before();
@@ -558,6 +598,12 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
             dw[c][e / 2 + 1] = pack_bf16(ds2, ds3);
           }
           tmem_st16(tmem + lane_base + 128 + q0, dw[c]);
+          if (SPL && c == 0) {
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars.dst_part);
+          }
         }
         tmem_st_wait();
         tc_fence_before();
@@ -620,14 +666,14 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D, int MODE, int PX = 0>
+template <int D, int MODE, int PX = 0, int SPL = 0>
 static cudaError_t launch_bwd_q128(const BwdParams& p, cudaStream_t s) {
   constexpr int bytes = bwd2::Cfg<D, MODE>::kBytes;
   static_assert(bytes <= 232448, "backward shared memory exceeds 227 KB");
   cudaError_t e =
-      cudaFuncSetAttribute(fa_bwd_q128_kernel<D, MODE, PX>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(fa_bwd_q128_kernel<D, MODE, PX, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   dim3 grid((p.Tk + bwd2::BK - 1) / bwd2::BK, p.Hkv);
-  fa_bwd_q128_kernel<D, MODE, PX><<<grid, bwd2::kThreads, bytes, s>>>(p);
+  fa_bwd_q128_kernel<D, MODE, PX, SPL><<<grid, bwd2::kThreads, bytes, s>>>(p);
   return cudaGetLastError();
 }

@@ -78,7 +78,7 @@ struct FwdBars {
   uint64_t q_full;
   uint64_t k_full[fwd::KST], k_empty[fwd::KST];
   uint64_t v_full[fwd::VST], v_empty[fwd::VST];
-  uint64_t s_full[2], p_half[2], p_full[2], o_full[2];
+  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];
   uint32_t tmem_base;
   int n_live;
   int warp_cnt[12];
@@ -197,10 +197,11 @@ __device__ __forceinline__ void fwd_epilogue(const FwdParams& p, uint32_t tO, in
   }
 }
 
-// SPLIT: the softmax releases P in two halves (keys 0-63, then 64-127) so the
-// first half of PV starts while it still computes the second (PV's K steps
-// run over keys); the O rescale moves before the exps to keep that legal.
-template <int D, bool SPLIT>
+// NP: the softmax releases P in NP parts of BN/NP keys (1, 2 or 4) so PV's K
+// steps (which run over keys) on the released parts start while it still
+// computes the rest; the O rescale moves before the exps to keep that legal.
+// p_part completes NP-1 times per iteration, p_full once.
+template <int D, int NP>
 __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_constant__ FwdParams p) {
   using namespace fwd;
   using L = FwdSmem<D>;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
     for (int i = 0; i < VST; ++i) { mbar_init(&bars.v_full[i], 1); mbar_init(&bars.v_empty[i], 1); }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars.s_full[t], 1);
-      mbar_init(&bars.p_half[t], 128);
+      mbar_init(&bars.p_part[t], 128);
       mbar_init(&bars.p_full[t], 128);
       mbar_init(&bars.o_full[t], 1);
     }
@@ -328,11 +329,11 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         FWAIT(&bars.v_full[vs], (it / VST) & 1, 0);
         const bool more = it + 1 < n;
         const int ks1 = (it + 1) % KST;
-        if (SPLIT) {  // keys 0-63 of P_0 while the softmax still produces 64-127
-          FWAIT(&bars.p_half[0], it & 1, 1);
+        for (int part = 0; part < NP - 1; ++part) {  // released parts of P_0 while the rest is computed
+          FWAIT(&bars.p_part[0], (it * (NP - 1) + part) & 1, 1);
           tc_fence_after();
           __syncwarp();
-          if (elect_one()) issue_pv(0, vs, it > 0, 0, BN / 32);
+          if (elect_one()) issue_pv(0, vs, it > 0, part * BN / 16 / NP, (part + 1) * BN / 16 / NP);
           __syncwarp();
         }
         FWAIT(&bars.p_full[0], it & 1, 1);
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
-          issue_pv(0, vs, it > 0, SPLIT ? BN / 32 : 0, BN / 16);
+          issue_pv(0, vs, it > 0, (NP - 1) * BN / 16 / NP, BN / 16);
           if (more) {
             issue_qk(0, ks1);
             umma_commit(&bars.s_full[0]);
@@ -349,18 +350,18 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           }
         }
         __syncwarp();
-        if (SPLIT) {
-          FWAIT(&bars.p_half[1], it & 1, 3);
+        for (int part = 0; part < NP - 1; ++part) {
+          FWAIT(&bars.p_part[1], (it * (NP - 1) + part) & 1, 3);
           tc_fence_after();
           __syncwarp();
-          if (elect_one()) issue_pv(1, vs, it > 0, 0, BN / 32);
+          if (elect_one()) issue_pv(1, vs, it > 0, part * BN / 16 / NP, (part + 1) * BN / 16 / NP);
           __syncwarp();
         }
         FWAIT(&bars.p_full[1], it & 1, 3);
         tc_fence_after();
         __syncwarp();
         if (elect_one()) {
-          issue_pv(1, vs, it > 0, SPLIT ? BN / 32 : 0, BN / 16);
+          issue_pv(1, vs, it > 0, (NP - 1) * BN / 16 / NP, BN / 16);
           umma_commit(&bars.v_empty[vs]);
           if (more) {
             issue_qk(1, ks1);
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
       }
       if (__any_sync(0xffffffffu, rescale)) {
         // O (this tile's previous PV) is complete: s_full's commit tracks it.
-        // Rescaled before P is released (SPLIT lets PV start on half of P).
+        // Rescaled before any part of P is released (PV starts on parts).
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
@@ -481,10 +482,10 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
           pk[(c - cc) / 2] = pack_bf16(e.x, e.y);
         }
         tmem_st16(tS + cc / 2, pk);
-        if (SPLIT && cc == BN / 2 - 32) {  // keys [0, BN/2) of P are in TMEM (and O is rescaled)
+        if (NP > 1 && cc + 32 < BN && (cc + 32) % (BN / NP) == 0) {  // a part of P is in TMEM
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&bars.p_half[t]);
+          mbar_arrive(&bars.p_part[t]);
         }
       }
       {
@@ -513,20 +514,20 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D, bool SPLIT>
+template <int D, int NP>
 static cudaError_t launch_fwd_d(const FwdParams& p, cudaStream_t s) {
   if ((p.Tk + fwd::BN - 1) / fwd::BN > fwd::kMaxKTiles) return cudaErrorInvalidValue;
   const int smem = FwdSmem<D>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int nqb = (p.Tq + 255) / 256;
   dim3 grid(nqb, p.H);
-  fa_fwd_kernel<D, SPLIT><<<grid, fwd::kThreads, smem, s>>>(p);
+  fa_fwd_kernel<D, NP><<<grid, fwd::kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 // Experiment switch (A2D_FWD_VARIANT, read once): 0 default (P released in
-// two halves), 1 = P released once (round 2).
+// two halves), 1 = P released once (round 2), 2 = in four quarters.
 static int fwd_variant() {
   static int v = -1;
   if (v < 0) {
@@ -538,9 +539,11 @@ static int fwd_variant() {
 
 cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s) {
   if (p.Tq <= 0 || p.H <= 0) return cudaSuccess;
-  const bool split = fwd_variant() != 1;
-  if (head_dim == 128) return split ? launch_fwd_d<128, true>(p, s) : launch_fwd_d<128, false>(p, s);
-  if (head_dim == 64) return split ? launch_fwd_d<64, true>(p, s) : launch_fwd_d<64, false>(p, s);
+  const int v = fwd_variant();
+  if (head_dim == 128)
+    return v == 1 ? launch_fwd_d<128, 1>(p, s) : v == 2 ? launch_fwd_d<128, 4>(p, s) : launch_fwd_d<128, 2>(p, s);
+  if (head_dim == 64)
+    return v == 1 ? launch_fwd_d<64, 1>(p, s) : v == 2 ? launch_fwd_d<64, 4>(p, s) : launch_fwd_d<64, 2>(p, s);
   return cudaErrorInvalidValue;
 }
 
