@@ -78,7 +78,7 @@ struct FwdBars {
   uint64_t q_full;
   uint64_t k_full[fwd::KST], k_empty[fwd::KST];
   uint64_t v_full[fwd::VST], v_empty[fwd::VST];
-  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];
+  uint64_t s_full[2], p_part[2][3], p_full[2], o_full[2];
   uint32_t tmem_base;
   int n_live;
   int warp_cnt[12];
@@ -200,7 +200,9 @@ __device__ __forceinline__ void fwd_epilogue(const FwdParams& p, uint32_t tO, in
 // NP: the softmax releases P in NP parts of BN/NP keys (1, 2 or 4) so PV's K
 // steps (which run over keys) on the released parts start while it still
 // computes the rest; the O rescale moves before the exps to keep that legal.
-// p_part completes NP-1 times per iteration, p_full once.
+// One barrier per part (each completes once per iteration: a barrier that
+// completed twice before its waiter looked would alias its parity), p_full
+// for the last.
 template <int D, int NP>
 __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_constant__ FwdParams p) {
   using namespace fwd;
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
     for (int i = 0; i < VST; ++i) { mbar_init(&bars.v_full[i], 1); mbar_init(&bars.v_empty[i], 1); }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars.s_full[t], 1);
-      mbar_init(&bars.p_part[t], 128);
+      for (int q = 0; q < 3; ++q) mbar_init(&bars.p_part[t][q], 128);
       mbar_init(&bars.p_full[t], 128);
       mbar_init(&bars.o_full[t], 1);
     }
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         const bool more = it + 1 < n;
         const int ks1 = (it + 1) % KST;
         for (int part = 0; part < NP - 1; ++part) {  // released parts of P_0 while the rest is computed
-          FWAIT(&bars.p_part[0], (it * (NP - 1) + part) & 1, 1);
+          FWAIT(&bars.p_part[0][part], it & 1, 1);
           tc_fence_after();
           __syncwarp();
           if (elect_one()) issue_pv(0, vs, it > 0, part * BN / 16 / NP, (part + 1) * BN / 16 / NP);
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         }
         __syncwarp();
         for (int part = 0; part < NP - 1; ++part) {
-          FWAIT(&bars.p_part[1], (it * (NP - 1) + part) & 1, 3);
+          FWAIT(&bars.p_part[1][part], it & 1, 3);
           tc_fence_after();
           __syncwarp();
           if (elect_one()) issue_pv(1, vs, it > 0, part * BN / 16 / NP, (part + 1) * BN / 16 / NP);
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         if (NP > 1 && cc + 32 < BN && (cc + 32) % (BN / NP) == 0) {  // a part of P is in TMEM
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&bars.p_part[t]);
+          mbar_arrive(&bars.p_part[t][(cc + 32) / (BN / NP) - 1]);
         }
       }
       {
@@ -527,7 +529,8 @@ static cudaError_t launch_fwd_d(const FwdParams& p, cudaStream_t s) {
 }
 
 // Experiment switch (A2D_FWD_VARIANT, read once): 0 default (P released in
-// two halves), 1 = P released once (round 2), 2 = in four quarters.
+// four quarters: 1310 vs 1287 TFLOP/s for halves, 1238 for once, sustained
+// S = 128K), 1 = P released once (round 2), 2 = in two halves.
 static int fwd_variant() {
   static int v = -1;
   if (v < 0) {
@@ -541,9 +544,9 @@ cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s) {
   if (p.Tq <= 0 || p.H <= 0) return cudaSuccess;
   const int v = fwd_variant();
   if (head_dim == 128)
-    return v == 1 ? launch_fwd_d<128, 1>(p, s) : v == 2 ? launch_fwd_d<128, 4>(p, s) : launch_fwd_d<128, 2>(p, s);
+    return v == 1 ? launch_fwd_d<128, 1>(p, s) : v == 2 ? launch_fwd_d<128, 2>(p, s) : launch_fwd_d<128, 4>(p, s);
   if (head_dim == 64)
-    return v == 1 ? launch_fwd_d<64, 1>(p, s) : v == 2 ? launch_fwd_d<64, 4>(p, s) : launch_fwd_d<64, 2>(p, s);
+    return v == 1 ? launch_fwd_d<64, 1>(p, s) : v == 2 ? launch_fwd_d<64, 2>(p, s) : launch_fwd_d<64, 4>(p, s);
   return cudaErrorInvalidValue;
 }
 
