@@ -12,6 +12,6 @@ timeout 600 python bench.py --runtime native --no-check > gpurun_out/g1_bench_na
 timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-check --no-cpu > gpurun_out/g1_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/g1_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-check --no-cpu > gpurun_out/g1_ncu_launch.log 2>&1; echo ncu1=$?
 timeout 300 python tools/kbench.py --S 131072 --iters 1 > gpurun_out/g1_kb_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fa_bwd_q128_kernel -c 1 -o gpurun_out/g1_fa_bwd python tools/kbench.py --S 131072 --iters 1 > gpurun_out/g1_ncu_bwd.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fa_fwd_kernel -c 1 -o gpurun_out/g1_fa_fwd python tools/kbench.py --S 131072 --iters 1 > gpurun_out/g1_ncu_fwd.log 2>&1; echo ncu2=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fa_bwd_q128_kernel -c 1 -o gpurun_out/g1_fa_bwd -f python tools/kbench.py --S 131072 --iters 1 > gpurun_out/g1_ncu_bwd.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fa_fwd_kernel -c 1 -o gpurun_out/g1_fa_fwd -f python tools/kbench.py --S 131072 --iters 1 > gpurun_out/g1_ncu_fwd.log 2>&1; echo ncu2=$?
 tail -3 gpurun_out/g1_pytest.log
