@@ -51,7 +51,6 @@ __device__ int g_bwd_ablate;
 // [kTraceIt0, kTraceIt0 + 32), 16 event slots each (tools/bwd_prof.py --trace)
 constexpr int kTraceIt0 = 200;
 __device__ long long g_bwd_trace[32 * 16];
-__device__ long long g_bwd_trace2[32 * 4];  // observer warp: s_full, dp_full, dq_full, p_full completion
 #define TR(slot, iter)                                                                                  \
   do {                                                                                                 \
     if (blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && (iter) >= kTraceIt0 && (iter) < kTraceIt0 + 32) \
@@ -635,8 +634,7 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
 
 #ifdef A2D_PROFILE
 extern "C" int a2d_prof_trace(long long* out) {
-  if (cudaMemcpyFromSymbol(out, a2d::g_bwd_trace, sizeof(long long) * 32 * 16) != cudaSuccess) return 2;
-  return cudaMemcpyFromSymbol(out + 32 * 16, a2d::g_bwd_trace2, sizeof(long long) * 32 * 4) == cudaSuccess ? 0 : 2;
+  return cudaMemcpyFromSymbol(out, a2d::g_bwd_trace, sizeof(long long) * 32 * 16) == cudaSuccess ? 0 : 2;
 }
 extern "C" int a2d_prof_ablate(int bits) {
   return cudaMemcpyToSymbol(a2d::g_bwd_ablate, &bits, sizeof(int)) == cudaSuccess ? 0 : 2;

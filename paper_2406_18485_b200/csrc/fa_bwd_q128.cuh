@@ -16,7 +16,7 @@
 //   R_S  [0,128)    S^T_i (keys x queries)  -> P^T_i  (bf16, TS A of dV)
 //   R_dP [128,256)  dP^T_i                  -> dS^T_i (bf16, TS A of dK)
 //                                           -> dQ^T_i = K^T dS^T_i (M = d)
-//   [256,384) dV,   [384,512) dK accumulators.
+//   [256,256+D) dV,   [256+D,256+2D) dK accumulators.
 // Issue order per iteration:  dV_i, S_{i+1}, dK_i, dQ^T_i, dP_{i+1}.
 //   S_{i+1} overwrites P^T_i right after dV_i (its only reader) and
 //   dQ^T_i overwrites dS^T_i right after dK_i: tcgen05.mma ops of one thread
@@ -24,10 +24,11 @@
 //   for S^T_{i+2} over P^T_i). S_{i+1} is issued before dK_i/dQ^T_i so the
 //   softmax of i+1 (MUFU-bound, ~1000 clk) runs under three GEMMs; the only
 //   exposed hand-off is the dQ^T drain's TMEM read before dP_{i+1}.
-// Shared memory (D = 128): K 32 KB, V 32 KB, 2 Q/dO stages 128 KB, dS^T
-// 32 KB = 224 KB; the dS^T buffer doubles as the dQ^T drain's staging (it is
-// free between dQ^T_i's completion and the softmax's dS_{i+1} store, which
-// waits for the drain). The live query-tile list is a bitmask (2 x 128 B).
+// Shared memory (D = 128, default staging): K 32 KB, V 32 KB, 2 Q stages
+// 64 KB, 1 dO stage 32 KB, dS^T 32 KB, dQ^T drain staging 32 KB = 224 KB (the
+// MODE comments below list the alternatives that were measured). The live
+// query-tile list is a bitmask (2 x 128 B). D = 64: same structure, dK at
+// column 320, dQ^T rows 64-127 unused.
 // Warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4-11 two P/dS
 // warpgroups (warpgroup hq owns queries [64hq, 64hq+64) of every iteration,
 // all 128 keys = TMEM lanes), 12-15 the dQ^T drain (TMEM lane = feature d).
@@ -228,25 +229,6 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
     }
     PFLUSH(3);
   }
-#ifdef A2D_PROFILE
-  else if (warp == 3) {
-    // observer: completion times of the commit / hand-off barriers (CTA 0 only)
-    if (blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) {
-      uint64_t* bs[4] = {&bars.s_full, &bars.dp_full, &bars.dq_full, &bars.p_full};
-      int nxt[4] = {0, 0, 0, 0};
-      const int lim = min(n, kTraceIt0 + 32);
-      while (nxt[0] < lim || nxt[1] < lim || nxt[2] < lim || nxt[3] < lim) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (nxt[k] < lim && mbar_test_wait(bs[k], nxt[k] & 1)) {
-            if (nxt[k] >= kTraceIt0) g_bwd_trace2[(nxt[k] - kTraceIt0) * 4 + k] = clock64();
-            ++nxt[k];
-          }
-        }
-      }
-    }
-  }
-#endif
   else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
     PSTART();

@@ -110,15 +110,13 @@ def main():
         res[role] = {slots[role][i]: round(vals[i] / tot, 4) for i in range(7) if slots[role][i] != "-"}
         res[role]["total_Gcycles"] = vals[7] / 1e9
     if os.environ.get("A2D_TRACE"):
-        tb = (ctypes.c_longlong * 640)()
+        tb = (ctypes.c_longlong * 512)()
         lib.a2d_prof_trace(tb)
         names = ["mma:dV(i)", "mma:S(i+1)", "mma:dK(i)", "mma:dQ(i)", "mma:dq_empty", "mma:dP(i+1)",
                  "sm:s_full", "sm:P_done", "sm:dp_full", "sm:dS_done", "sm:sts_start", "sm:sts_done",
                  "sm1:P_done", "dr:dq_full", "dr:dq_empty", "dr:end"]
         t0 = tb[0]
         res["trace_cycles_rel_to_first_dV"] = {n: [tb[i * 16 + k] - t0 for i in range(32)] for k, n in enumerate(names)}
-        for k, n in enumerate(["ob:s_full", "ob:dp_full", "ob:dq_full", "ob:p_full"]):
-            res["trace_cycles_rel_to_first_dV"][n] = [tb[512 + i * 4 + k] - t0 for i in range(32)]
         per = [(tb[(i + 1) * 16] - tb[i * 16]) for i in range(31)]
         res["trace_period"] = per
     print(json.dumps(res, indent=1))
