@@ -203,7 +203,8 @@ __device__ __forceinline__ void fwd_epilogue(const FwdParams& p, uint32_t tO, in
 // One barrier per part (each completes once per iteration: a barrier that
 // completed twice before its waiter looked would alias its parity), p_full
 // for the last.
-template <int D, int NP>
+// PXF: exp2 pairs on the FMA pipe out of every eight (0, 1, 2 = the default 1/4, 3).
+template <int D, int NP, int PXF = 2>
 __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_constant__ FwdParams p) {
   using namespace fwd;
   using L = FwdSmem<D>;
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
         for (int c = cc; c < cc + 32; c += 2) {
           const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl2x2, nm2);
           float2 e;
-          if (((c / 2) & 3) == 3) {  // one pair in four on the FMA pipe (MUFU relief)
+          if (((c / 2) & 7) >= 8 - PXF) {  // PXF pairs in eight on the FMA pipe (MUFU relief)
             e = ex2_poly2(x);
           } else {
             e.x = ex2(x.x);
@@ -516,21 +517,22 @@ __global__ void __launch_bounds__(fwd::kThreads, 1) fa_fwd_kernel(const __grid_c
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D, int NP>
+template <int D, int NP, int PXF = 2>
 static cudaError_t launch_fwd_d(const FwdParams& p, cudaStream_t s) {
   if ((p.Tk + fwd::BN - 1) / fwd::BN > fwd::kMaxKTiles) return cudaErrorInvalidValue;
   const int smem = FwdSmem<D>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(fa_fwd_kernel<D, NP, PXF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int nqb = (p.Tq + 255) / 256;
   dim3 grid(nqb, p.H);
-  fa_fwd_kernel<D, NP><<<grid, fwd::kThreads, smem, s>>>(p);
+  fa_fwd_kernel<D, NP, PXF><<<grid, fwd::kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 // Experiment switch (A2D_FWD_VARIANT, read once): 0 default (P released in
 // four quarters: 1310 vs 1287 TFLOP/s for halves, 1238 for once, sustained
-// S = 128K), 1 = P released once (round 2), 2 = in two halves.
+// S = 128K), 1 = P released once (round 2), 2 = in two halves; 3 / 4 / 5 =
+// quarters with 0 / 1/8 / 3/8 of the exp pairs on the FMA pipe (default 1/4).
 static int fwd_variant() {
   static int v = -1;
   if (v < 0) {
@@ -544,7 +546,12 @@ cudaError_t launch_fa_fwd(const FwdParams& p, int head_dim, cudaStream_t s) {
   if (p.Tq <= 0 || p.H <= 0) return cudaSuccess;
   const int v = fwd_variant();
   if (head_dim == 128)
-    return v == 1 ? launch_fwd_d<128, 1>(p, s) : v == 2 ? launch_fwd_d<128, 2>(p, s) : launch_fwd_d<128, 4>(p, s);
+    return v == 1   ? launch_fwd_d<128, 1>(p, s)
+           : v == 2 ? launch_fwd_d<128, 2>(p, s)
+           : v == 3 ? launch_fwd_d<128, 4, 0>(p, s)
+           : v == 4 ? launch_fwd_d<128, 4, 1>(p, s)
+           : v == 5 ? launch_fwd_d<128, 4, 3>(p, s)
+                    : launch_fwd_d<128, 4>(p, s);
   if (head_dim == 64)
     return v == 1 ? launch_fwd_d<64, 1>(p, s) : v == 2 ? launch_fwd_d<64, 2>(p, s) : launch_fwd_d<64, 4>(p, s);
   return cudaErrorInvalidValue;
