@@ -103,7 +103,7 @@ def main():
     lib.a2d_prof_read(buf, 32)
     ms = e0.elapsed_time(e1)
     res = {"shape": vars(a), "bwd_ms": ms, "bwd_tflops": 2.5 * 2.0 * S * S * H * d / ms / 1e9}
-    slots = SLOTS_Q128 if d == 128 and os.environ.get("A2D_BWD_VARIANT", "0") in ("0", "7", "8", "9", "10") else SLOTS
+    slots = SLOTS_Q128 if d == 128 and os.environ.get("A2D_BWD_VARIANT", "0") in ("0", "7", "8", "9", "10", "11", "13") else SLOTS
     for role, base in (("mma", 0), ("pds", 8), ("drain", 16), ("tma", 24)):
         vals = list(buf[base:base + 8])
         tot = vals[7] or 1
