@@ -593,9 +593,12 @@ static cudaError_t launch_bwd_d(const BwdParams& p, cudaStream_t s) {
 }
 
 // Experiment switch (A2D_BWD_VARIANT, read once): 0 default (the 128-query
-// kernel, fa_bwd_q128.cuh, own drain staging, D = 64 or 128), 7 / 8 = the 128-query kernel with the kStageDs /
+// kernel, fa_bwd_q128.cuh, own drain staging, CTA pairs with multicast Q/dO
+// loads (single CTAs when the key-tile count is odd), D = 64 or 128), 15 =
+// the same without pairs, 7 / 8 = the 128-query kernel with the kStageDs /
 // kStageHybrid drain staging, 9 / 10 = own staging with 1/8 / 1/4 of the
-// P exps on the FMA pipe, 11 = P^T / dS^T released in two parts, 6 = the round-2
+// P exps on the FMA pipe (7-11 without pairs), 11 = P^T / dS^T released in
+// two parts, 6 = the round-2
 // 64-query kernel at D = 128 (3 stages, no prefetch), 1 = it with 2 stages,
 // 2 = L2 prefetch 4 ahead, 3 = L2 prefetch 8 ahead, 4 = 4 stages with the
 // per-warp 8-query dQ drain, 5 = 3 stages with it.
@@ -613,7 +616,9 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
   if (p.Tk <= 0 || p.Hkv <= 0) return cudaSuccess;
   if ((p.Tq + bwd::BQ - 1) / bwd::BQ > bwd::kMaxQTiles) return cudaErrorInvalidValue;
   if (head_dim == 64)
-    return bwd_variant() == 6 ? launch_bwd_d<64, 3, 0>(p, s) : launch_bwd_q128<64, bwd2::kStageOwn>(p, s);
+    return bwd_variant() == 6    ? launch_bwd_d<64, 3, 0>(p, s)
+           : bwd_variant() == 15 ? launch_bwd_q128<64, bwd2::kStageOwn>(p, s)
+                                 : launch_bwd_q128<64, bwd2::kStageOwn, 0, 0, true>(p, s);
   switch (bwd_variant()) {
     case 1: return launch_bwd_d<128, 2, 0>(p, s);
     case 2: return launch_bwd_d<128, 3, 4>(p, s);
@@ -626,7 +631,8 @@ cudaError_t launch_fa_bwd(const BwdParams& p, int head_dim, cudaStream_t s) {
     case 9: return launch_bwd_q128<128, bwd2::kStageOwn, 1>(p, s);
     case 10: return launch_bwd_q128<128, bwd2::kStageOwn, 2>(p, s);
     case 11: return launch_bwd_q128<128, bwd2::kStageOwn, 0, 1>(p, s);
-    default: return launch_bwd_q128<128, bwd2::kStageOwn>(p, s);
+    case 15: return launch_bwd_q128<128, bwd2::kStageOwn>(p, s);
+    default: return launch_bwd_q128<128, bwd2::kStageOwn, 0, 0, true>(p, s);
   }
 }
 

@@ -98,7 +98,12 @@ struct LiveIt {
 // (128 x 128 exps per iteration = 1024 MUFU clk) and gates dV.
 // SPL: the P/dS warps release P^T and dS^T in two parts (their first 32-query
 // chunk, then the second), so dV / dK start on half of the K steps early.
-template <int D, int MODE, int PX, int SPL>
+// CL: CTA pairs (cluster of 2 along the key tiles, an even number of them):
+// both CTAs walk the union of their live query tiles; rank 0 loads each Q
+// tile and rank 1 each dO tile with TMA multicast into both CTAs, halving the
+// SM's L1->L2 load requests (the path the dQ^T reduces saturate). A stage is
+// refilled once both CTAs' MMAs released it (multicast commits, count 2).
+template <int D, int MODE, int PX, int SPL, bool CL = false>
 __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __grid_constant__ BwdParams p) {
   using namespace bwd2;
   using C = Cfg<D, MODE>;
@@ -120,13 +125,15 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
   const int nwords = (nqt + 31) / 32;
   const int Tq_pad = p.stats_stride;
   const int2 kb = p.k_bounds[kt];
+  const int2 kb_peer = CL ? p.k_bounds[kt ^ 1] : kb;
   const bool causal = p.causal != 0;
+  const uint32_t crank = CL ? cluster_rank() : 0u;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
     for (int i = 0; i < QST; ++i) {
-      mbar_init(&bars.q_full[i], 1); mbar_init(&bars.q_empty[i], 1);
-      mbar_init(&bars.do_full[i], 1); mbar_init(&bars.do_empty[i], 1);
+      mbar_init(&bars.q_full[i], 1); mbar_init(&bars.q_empty[i], CL ? 2 : 1);
+      mbar_init(&bars.do_full[i], 1); mbar_init(&bars.do_empty[i], CL ? 2 : 1);
     }
     mbar_init(&bars.s_full, 1);
     mbar_init(&bars.dp_full, 1);
@@ -160,6 +167,8 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
         qb = make_int2(min(qb.x, b1.x), max(qb.y, b1.y));
       }
       lv = qb.x <= qb.y && kb.x <= kb.y && (!causal || kb.x <= qb.y);
+      if (CL)  // the pair walks the union (a tile dead here is never full: masked to P = 0)
+        lv = lv || (qb.x <= qb.y && kb_peer.x <= kb_peer.y && (!causal || kb_peer.x <= qb.y));
       // full: no mask needed. A tile reaching past the 64-padded stats
       // (single 64-row half) is always masked.
       full = two && (!causal || kb.y <= qb.x);
@@ -169,6 +178,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
   }
   tc_fence_before();
   __syncthreads();
+  if (CL) cluster_sync();  // both CTAs' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
   int n_live = 0;
@@ -212,18 +222,28 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
           const int nst = (2 * qt + 1 < nqt64) ? BQ : 64;
           mbar_expect_tx(&bars.q_full[qs], C::kQStage + 2 * nst * 4);
           uint8_t* sq = smem + kQ + qs * C::kQStage;
-          for (int c = 0; c < C::kPanels; ++c)
-            for (int hh = 0; hh < 2; ++hh)
-              tma_load_3d(sq + c * 16384 + hh * 8192, &p.tm_q, &bars.q_full[qs], c * 64, qt * BQ + hh * 64, h);
+          if (!CL || crank == 0)
+            for (int c = 0; c < C::kPanels; ++c)
+              for (int hh = 0; hh < 2; ++hh) {
+                if (CL)
+                  tma_load_3d_mc(sq + c * 16384 + hh * 8192, &p.tm_q, &bars.q_full[qs], c * 64, qt * BQ + hh * 64, h, 3);
+                else
+                  tma_load_3d(sq + c * 16384 + hh * 8192, &p.tm_q, &bars.q_full[qs], c * 64, qt * BQ + hh * 64, h);
+              }
           float* st = reinterpret_cast<float*>(smem + kStats) + qs * 2 * BQ;
           bulk_g2s(st, p.lse2 + (size_t)h * Tq_pad + qt * BQ, nst * 4, &bars.q_full[qs]);
           bulk_g2s(st + BQ, p.delta + (size_t)h * Tq_pad + qt * BQ, nst * 4, &bars.q_full[qs]);
           PWAIT(&bars.do_empty[ds], ((it / NDO) & 1) ^ 1, 1);
           mbar_expect_tx(&bars.do_full[ds], C::kQStage);
           uint8_t* sd = smem + kDO + ds * C::kQStage;
-          for (int c = 0; c < C::kPanels; ++c)
-            for (int hh = 0; hh < 2; ++hh)
-              tma_load_3d(sd + c * 16384 + hh * 8192, &p.tm_do, &bars.do_full[ds], c * 64, qt * BQ + hh * 64, h);
+          if (!CL || crank == 1)
+            for (int c = 0; c < C::kPanels; ++c)
+              for (int hh = 0; hh < 2; ++hh) {
+                if (CL)
+                  tma_load_3d_mc(sd + c * 16384 + hh * 8192, &p.tm_do, &bars.do_full[ds], c * 64, qt * BQ + hh * 64, h, 3);
+                else
+                  tma_load_3d(sd + c * 16384 + hh * 8192, &p.tm_do, &bars.do_full[ds], c * 64, qt * BQ + hh * 64, h);
+              }
         }
       }
     }
@@ -302,7 +322,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
             if (!SPL || (k / 2) % 2 == 1)
               umma_ts(tDV, tS + (k / 2) * 32 + (k % 2) * 8, dDOmn + doff + (uint64_t)(k * 128), id_kv,
                       (i > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&bars.do_empty[ds]);  // dO_i's last reader
+          if (CL) umma_commit_mc(&bars.do_empty[ds], 3); else umma_commit(&bars.do_empty[ds]);  // dO_i's last reader
         }
         __syncwarp();
         // S^T_{i+1} into R_S (after dV_i in the in-order pipe)
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
             if (!SPL || (k / 2) % 2 == 1)
               umma_ts(tDK, tDP + (k / 2) * 32 + (k % 2) * 8, dQmn + qoff + (uint64_t)(k * 128), id_kv,
                       (i > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&bars.q_empty[qs]);
+          if (CL) umma_commit_mc(&bars.q_empty[qs], 3); else umma_commit(&bars.q_empty[qs]);
         }
         __syncwarp();
         // dQ^T_i = K^T dS^T_i into R_dP (after dK_i); dS^T from shared memory
@@ -645,17 +665,32 @@ __global__ void __launch_bounds__(bwd2::kThreads, 1) fa_bwd_q128_kernel(const __
 
   tc_fence_before();
   __syncthreads();
+  if (CL) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int D, int MODE, int PX = 0, int SPL = 0>
+template <int D, int MODE, int PX = 0, int SPL = 0, bool CL = false>
 static cudaError_t launch_bwd_q128(const BwdParams& p, cudaStream_t s) {
   constexpr int bytes = bwd2::Cfg<D, MODE>::kBytes;
   static_assert(bytes <= 232448, "backward shared memory exceeds 227 KB");
-  cudaError_t e =
-      cudaFuncSetAttribute(fa_bwd_q128_kernel<D, MODE, PX, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  auto kern = fa_bwd_q128_kernel<D, MODE, PX, SPL, CL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.Tk + bwd2::BK - 1) / bwd2::BK, p.Hkv);
-  fa_bwd_q128_kernel<D, MODE, PX, SPL><<<grid, bwd2::kThreads, bytes, s>>>(p);
+  const int nkt = (p.Tk + bwd2::BK - 1) / bwd2::BK;
+  if (CL && (nkt % 2) != 0) return launch_bwd_q128<D, MODE, PX, SPL, false>(p, s);  // pairs need an even count
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nkt, p.Hkv);
+  cfg.blockDim = dim3(bwd2::kThreads);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CL ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

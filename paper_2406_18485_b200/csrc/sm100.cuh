@@ -150,6 +150,25 @@ A2D_DEV void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_clus
       : "memory");
 }
 
+// Multicast load: lands at the same smem offset in every CTA of `mask` and
+// completes bytes on the mbarrier at the same offset in each of them.
+A2D_DEV void tma_load_3d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+// Arrive (once this thread's prior tcgen05 ops complete) on the barrier at
+// this smem offset in every CTA of `mask` (single-CTA MMAs).
+A2D_DEV void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05
 // CTA-pair (cta_group::2) variants — validated on B200 by the pair forward
 // experiment; building blocks for a pair backward. The same warp id of both CTAs allocates /
