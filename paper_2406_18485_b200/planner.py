@@ -29,8 +29,8 @@ class B200Calibration:
     """Measured on B200 (round 1): tools/kbench.py, bench.py sweeps, tools/trace.py
     phase traces (profiles/r01_trace_*.json), guide peaks."""
 
-    fwd_tflops: float = 1195.0     # forward chunk kernel in a full step (round-2b build)
-    bwd_tflops: float = 1110.0     # backward chunk kernel in a full step (round-2b 128-query kernel)
+    fwd_tflops: float = 1310.0     # forward chunk kernel in a full step (final round-2b build: P in quarters)
+    bwd_tflops: float = 1135.0     # backward chunk kernel in a full step (128-query kernel, CTA pairs)
     short_chunk_tokens: float = 500.0   # kernel efficiency ~ C / (C + this) for small chunks
     a2a_gbs: float = 620.0         # NCCL all_to_all_single: time ~ whole buffer / this (traces, d_hp = 2 and 4)
     ce_gbs: float = 770.0          # copy-engine write into a peer's symmetric buffer (tools/probes/peer_probe.py)
@@ -54,6 +54,9 @@ EARLY_ROUND1 = B200Calibration(fwd_tflops=1100.0, bwd_tflops=940.0, transport="n
 # The final round-1 / round-2 builds (64-query backward) that produced
 # profiles/r01_final_sweep_S128k_symm_2_4gpu.jsonl.
 ROUND2 = B200Calibration(fwd_tflops=1180.0, bwd_tflops=1040.0)
+# The first round-2b build (128-query backward without pairs, forward P
+# released once) that produced profiles/r02b_sweep_S128k_4gpu.jsonl.
+ROUND2B_SWEEP = B200Calibration(fwd_tflops=1195.0, bwd_tflops=1110.0)
 
 
 def _eff(c: B200Calibration, tokens: int) -> float:

@@ -13,7 +13,7 @@ from paper_2406_18485_b200.config import ModelConfig, ParallelConfig, Placement
 SWEEPS = [(os.path.join(ROOT, "profiles", "r01_sweep_S128k_2_4gpu.jsonl"), P.EARLY_ROUND1, 18),
           (os.path.join(ROOT, "profiles", "r01_sweep_S512k_2_4gpu.jsonl"), P.EARLY_ROUND1, 18),
           (os.path.join(ROOT, "profiles", "r01_final_sweep_S128k_symm_2_4gpu.jsonl"), P.ROUND2, 9),
-          (os.path.join(ROOT, "profiles", "r02b_sweep_S128k_4gpu.jsonl"), P.calibration(), 6)]
+          (os.path.join(ROOT, "profiles", "r02b_sweep_S128k_4gpu.jsonl"), P.ROUND2B_SWEEP, 6)]
 REF_SRC = os.environ.get("ATTN2D_REF", "/root/reference/pkg/src")
 
 
