@@ -568,7 +568,7 @@ def main():
                 traffic = tr
         except (OSError, ValueError):
             pass
-        roof = {"kernel": "a2d_fa_bwd_chunk (fa_bwd_q128_kernel at d=128, fa_bwd_kernel at d=64)", "bound": "tensor",
+        roof = {"kernel": "a2d_fa_bwd_chunk (fa_bwd_q128_kernel, CTA pairs)", "bound": "tensor",
                 "achieved": bwd_achieved, "peak": pk["bf16_tflops_sustained"], "unit": UNIT,
                 "frac": (bwd_achieved / pk["bf16_tflops_sustained"]) if bwd_achieved else None,
                 "frac_of_burst": (bwd_achieved / pk["bf16_tflops"]) if bwd_achieved else None,
